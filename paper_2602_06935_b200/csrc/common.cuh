@@ -1,0 +1,83 @@
+// Shared definitions for the cosine-attention kernels (sm_100a).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cotten {
+
+// Everything a forward or backward launch needs for the whole batch.  Units
+// are (sequence b, head h) pairs, unit = b*H + h; element (b,h,i,j) lives at
+// base[b*sb + h*sh + i*sn + j] (see include/cotten.h).
+struct OpParams {
+  const void* q;
+  const void* k;
+  const void* v;
+  const void* dout;
+  void* out;
+  void* dq;
+  void* dk;
+  void* dv;
+  const uint8_t* valid;  // [B][msb] bytes or nullptr
+  void* saved_S;         // [B*H][D][D] accumulation type or nullptr
+  void* saved_norms;     // [B*H][2][N] accumulation type or nullptr
+  double* dm_unit;       // [B*H] or nullptr
+  int* status;           // sticky per-device status word (COTTEN_STATUS_*)
+  int64_t B, H, N, D;
+  int64_t sb, sh, sn, msb;
+  double m, eps;
+};
+
+template <typename T>
+struct AccOf {
+  using type = float;
+};
+template <>
+struct AccOf<double> {
+  using type = double;
+};
+
+__device__ __forceinline__ float ld_acc(const float* p) { return *p; }
+__device__ __forceinline__ double ld_acc(const double* p) { return *p; }
+__device__ __forceinline__ float ld_acc(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+__device__ __forceinline__ void st_from(float* p, float x) { *p = x; }
+__device__ __forceinline__ void st_from(double* p, double x) { *p = x; }
+__device__ __forceinline__ void st_from(__nv_bfloat16* p, float x) { *p = __float2bfloat16_rn(x); }
+
+template <typename A>
+__device__ __forceinline__ A rsqrt_acc(A x);
+template <>
+__device__ __forceinline__ float rsqrt_acc<float>(float x) {
+  return 1.0f / sqrtf(x);  // IEEE sqrt + div: within 1 ulp of the fp64 reference
+}
+template <>
+__device__ __forceinline__ double rsqrt_acc<double>(double x) {
+  return 1.0 / sqrt(x);
+}
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+template <typename A>
+__device__ __forceinline__ A warp_sum(A x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Count of valid rows of sequence b (attention.cpp:26-33), computed by the
+// whole block; all threads get the result.
+__device__ __forceinline__ int64_t block_true_count(const OpParams& p, int64_t b, int* s_cnt) {
+  if (threadIdx.x == 0) *s_cnt = 0;
+  __syncthreads();
+  if (p.valid == nullptr) return p.N;
+  int c = 0;
+  const uint8_t* row = p.valid + b * p.msb;
+  for (int64_t i = threadIdx.x; i < p.N; i += blockDim.x) c += row[i] != 0;
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(s_cnt, c);
+  __syncthreads();
+  return *s_cnt;
+}
+
+}  // namespace cotten

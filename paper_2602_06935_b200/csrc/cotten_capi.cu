@@ -1,0 +1,488 @@
+// C-ABI of the cosine-attention operator (include/cotten.h): validation,
+// kernel dispatch, per-thread workspaces and the host-buffer entry points.
+// Error conventions mirror the reference C API (capi.cpp:21-44).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/cotten.h"
+#include "common.cuh"
+#include "kernels_d32.cuh"
+#include "kernels_generic.cuh"
+
+namespace cotten {
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_launches = 0;
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void usage(const std::string& what) { throw Error{COTTEN_ERR_USAGE, what}; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define COTTEN_CUDA(call)                                                                  \
+  do {                                                                                     \
+    cudaError_t err_ = (call);                                                             \
+    if (err_ != cudaSuccess)                                                               \
+      throw Error{COTTEN_ERR_INTERNAL, std::string(#call) + ": " + cudaGetErrorString(err_)}; \
+  } while (0)
+
+template <typename F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return COTTEN_OK;
+  } catch (const Error& e) {
+    return fail(e.code, e.msg);
+  } catch (const std::exception& e) {
+    return fail(COTTEN_ERR_INTERNAL, e.what());
+  } catch (...) {
+    return fail(COTTEN_ERR_INTERNAL, "unknown error");
+  }
+}
+
+
+size_t elem_size(int dtype) {
+  switch (dtype) {
+    case COTTEN_F32: return 4;
+    case COTTEN_BF16: return 2;
+    case COTTEN_F64: return 8;
+  }
+  usage("cotten: unknown dtype");
+}
+size_t acc_size(int dtype) { return dtype == COTTEN_F64 ? 8 : 4; }
+
+// Resolved, validated view of a cotten_desc (check_qkv, attention.cpp:37-46).
+struct Layout {
+  int64_t B, H, N, D, sb, sh, sn, msb;
+  int dtype, flags;
+  double eps;
+  int64_t units() const { return B * H; }
+  // Elements spanned by one tensor, for staging copies of the host API.
+  int64_t span() const { return (B - 1) * sb + (H - 1) * sh + (N - 1) * sn + D; }
+  // The host entry points copy whole spans, so they need a gap-free layout.
+  void require_dense(const char* what) const {
+    if (span() != B * H * N * D)
+      usage(std::string(what) + ": host entry points need a dense (gap-free) layout");
+  }
+};
+
+Layout resolve(const cotten_desc* d, const char* what) {
+  if (d == nullptr) usage(std::string(what) + ": null descriptor");
+  Layout L{};
+  L.B = d->batch;
+  L.H = d->heads;
+  L.N = d->seq_len;
+  L.D = d->head_dim;
+  L.dtype = d->dtype;
+  L.flags = d->flags;
+  L.eps = d->eps;
+  if (L.B < 1 || L.H < 1 || L.N < 1 || L.D < 1)
+    usage(std::string(what) + ": empty matrix (batch, heads, seq_len, head_dim must be >= 1)");
+  elem_size(L.dtype);
+  if (!(L.eps >= 0.0) || !std::isfinite(L.eps)) usage(std::string(what) + ": eps must be >= 0");
+  if (d->stride_b == 0 && d->stride_h == 0 && d->stride_n == 0) {
+    L.sn = L.D;
+    L.sh = L.N * L.D;
+    L.sb = L.H * L.N * L.D;
+  } else {
+    L.sb = d->stride_b;
+    L.sh = d->stride_h;
+    L.sn = d->stride_n;
+    if (L.sn < L.D || L.sh < 1 || L.sb < 1)
+      usage(std::string(what) + ": strides must be positive and stride_n >= head_dim");
+  }
+  L.msb = d->mask_stride_b == 0 ? L.N : d->mask_stride_b;
+  if (L.msb < L.N) usage(std::string(what) + ": mask length (mask_stride_b < seq_len)");
+  return L;
+}
+
+void check_generic_fits(const Layout& L, bool bwd) {
+  const size_t need = L.dtype == COTTEN_F64 ? (bwd ? gen_bwd_smem<double>(L.D) : gen_fwd_smem<double>(L.D))
+                                            : (bwd ? gen_bwd_smem<float>(L.D) : gen_fwd_smem<float>(L.D));
+  if (need > 227 * 1024)
+    usage("cotten: head_dim " + std::to_string(L.D) + " exceeds the shared-memory budget for dtype");
+}
+
+OpParams make_params(const Layout& L) {
+  OpParams p{};
+  p.B = L.B;
+  p.H = L.H;
+  p.N = L.N;
+  p.D = L.D;
+  p.sb = L.sb;
+  p.sh = L.sh;
+  p.sn = L.sn;
+  p.msb = L.msb;
+  p.eps = L.eps;
+  return p;
+}
+
+// ---- per-device state ---------------------------------------------------
+
+std::mutex g_dev_mu;
+std::vector<int*> g_status;  // one sticky status word per device
+
+int* device_status_word() {
+  int dev = 0;
+  COTTEN_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if ((int)g_status.size() <= dev) g_status.resize(dev + 1, nullptr);
+  if (g_status[dev] == nullptr) {
+    COTTEN_CUDA(cudaMalloc(&g_status[dev], sizeof(int)));
+    COTTEN_CUDA(cudaMemset(g_status[dev], 0, sizeof(int)));
+  }
+  return g_status[dev];
+}
+
+// Grow-only device scratch, one per (thread, device); used for per-unit dm
+// and a recomputed S when the caller passes none.  Allocation happens only
+// when a call needs more than any earlier call (never in steady state).
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int dev = -1;
+  void* get(size_t need) {
+    int cur = 0;
+    COTTEN_CUDA(cudaGetDevice(&cur));
+    if (dev != cur) {  // another device: drop our (stale) handle, allocate anew
+      ptr = nullptr;
+      bytes = 0;
+      dev = cur;
+    }
+    if (need > bytes) {
+      if (ptr) cudaFree(ptr);
+      ptr = nullptr;
+      COTTEN_CUDA(cudaMalloc(&ptr, need));
+      bytes = need;
+    }
+    return ptr;
+  }
+};
+thread_local Scratch g_dm_scratch, g_s_scratch;
+
+// ---- launches -------------------------------------------------------------
+
+template <typename T>
+void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
+  using A = typename AccOf<T>::type;
+  if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && fast_fwd_supported<T>(p)) {
+    g_launches += launch_fast_fwd<T>(p, st);
+  } else {
+    check_generic_fits(L, false);
+    const size_t smem = gen_fwd_smem<A>(L.D);
+    COTTEN_CUDA(cudaFuncSetAttribute(cos_fwd_generic<T, A>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cos_fwd_generic<T, A><<<(unsigned)L.units(), kGenThreads, smem, st>>>(p);
+    g_launches += 1;
+  }
+  COTTEN_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
+  using A = typename AccOf<T>::type;
+  if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && fast_bwd_supported<T>(p)) {
+    g_launches += launch_fast_bwd<T>(p, st);
+  } else {
+    check_generic_fits(L, true);
+    const size_t smem = gen_bwd_smem<A>(L.D);
+    COTTEN_CUDA(cudaFuncSetAttribute(cos_bwd_generic<T, A>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cos_bwd_generic<T, A><<<(unsigned)L.units(), kGenThreads, smem, st>>>(p);
+    g_launches += 1;
+  }
+  COTTEN_CUDA(cudaGetLastError());
+}
+
+void launch_fwd(const Layout& L, const OpParams& p, cudaStream_t st) {
+  switch (L.dtype) {
+    case COTTEN_F32: return launch_fwd_t<float>(L, p, st);
+    case COTTEN_BF16: return launch_fwd_t<__nv_bfloat16>(L, p, st);
+    case COTTEN_F64: return launch_fwd_t<double>(L, p, st);
+  }
+}
+void launch_bwd(const Layout& L, const OpParams& p, cudaStream_t st) {
+  switch (L.dtype) {
+    case COTTEN_F32: return launch_bwd_t<float>(L, p, st);
+    case COTTEN_BF16: return launch_bwd_t<__nv_bfloat16>(L, p, st);
+    case COTTEN_F64: return launch_bwd_t<double>(L, p, st);
+  }
+}
+
+void device_fwd(const Layout& L, const void* q, const void* k, const void* v,
+                const uint8_t* valid, double m, void* out, void* saved_S, void* saved_norms,
+                cudaStream_t st) {
+  if (!q || !k || !v) usage("cosine_attention_fused: null input");
+  if (!out && !saved_S && !saved_norms) usage("cosine_attention_fused: no output requested");
+  if (!std::isfinite(m)) usage("cosine_attention_fused: m must be finite");
+  OpParams p = make_params(L);
+  p.q = q;
+  p.k = k;
+  p.v = v;
+  p.valid = valid;
+  p.m = m;
+  p.out = out;
+  p.saved_S = saved_S;
+  p.saved_norms = saved_norms;
+  p.status = device_status_word();
+  launch_fwd(L, p, st);
+}
+
+void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
+                const uint8_t* valid, double m, const void* d_out, const void* saved_S, void* dq,
+                void* dk, void* dv, double* dm_unit, double* dm_total, cudaStream_t st) {
+  if (!q || !k || !v || !d_out) usage("cosine_attention_backward: null input");
+  if (!dq || !dk || !dv) usage("cosine_attention_backward: null gradient output");
+  if (!std::isfinite(m)) usage("cosine_attention_backward: m must be finite");
+  OpParams p = make_params(L);
+  p.q = q;
+  p.k = k;
+  p.v = v;
+  p.valid = valid;
+  p.m = m;
+  p.status = device_status_word();
+  if (saved_S == nullptr) {  // recompute the state with an S-only forward
+    void* s = g_s_scratch.get(L.units() * L.D * L.D * acc_size(L.dtype));
+    OpParams f = p;
+    f.saved_S = s;
+    launch_fwd(L, f, st);
+    saved_S = s;
+  }
+  p.saved_S = const_cast<void*>(saved_S);
+  p.dout = d_out;
+  p.dq = dq;
+  p.dk = dk;
+  p.dv = dv;
+  p.dm_unit = dm_unit;
+  if (dm_total && !dm_unit) p.dm_unit = static_cast<double*>(g_dm_scratch.get(L.units() * sizeof(double)));
+  launch_bwd(L, p, st);
+  if (dm_total) {
+    dm_reduce_kernel<<<1, 256, 0, st>>>(p.dm_unit, L.units(), dm_total);
+    g_launches += 1;
+    COTTEN_CUDA(cudaGetLastError());
+  }
+}
+
+// ---- host entry points ----------------------------------------------------
+
+// Mask check on the host, exactly check_qkv's (attention.cpp:42-45).
+void host_check_mask(const Layout& L, const uint8_t* valid, const char* what) {
+  if (valid == nullptr) return;
+  for (int64_t b = 0; b < L.B; ++b) {
+    const uint8_t* row = valid + b * L.msb;
+    int64_t c = 0;
+    for (int64_t i = 0; i < L.N; ++i) c += row[i] != 0;
+    if (c == 0) usage(std::string(what) + ": no real rows (sequence " + std::to_string(b) + ")");
+  }
+}
+
+// Per-thread staging state for the host entry points.
+struct HostCtx {
+  cudaStream_t stream = nullptr;
+  int dev = -1;
+  std::vector<void*> bufs;
+  std::vector<size_t> sizes;
+  ~HostCtx() {
+    // Process teardown may have destroyed the context already; ignore errors.
+    for (void* b : bufs)
+      if (b) cudaFree(b);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void ensure() {
+    int cur = 0;
+    COTTEN_CUDA(cudaGetDevice(&cur));
+    if (dev != cur) {
+      bufs.assign(12, nullptr);
+      sizes.assign(12, 0);
+      stream = nullptr;
+      dev = cur;
+    }
+    if (stream == nullptr) COTTEN_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  }
+  void* buf(int slot, size_t need) {
+    if (need > sizes[slot]) {
+      if (bufs[slot]) cudaFree(bufs[slot]);
+      bufs[slot] = nullptr;
+      COTTEN_CUDA(cudaMalloc(&bufs[slot], need));
+      sizes[slot] = need;
+    }
+    return bufs[slot];
+  }
+};
+thread_local HostCtx g_host;
+
+enum Slot { kQ, kK, kV, kO, kDO, kDQ, kDK, kDV, kMask, kS, kNorms, kDm };
+
+void* h2d(int slot, const void* src, size_t bytes) {
+  void* dst = g_host.buf(slot, bytes);
+  COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g_host.stream));
+  return dst;
+}
+void d2h(void* dst, const void* src, size_t bytes) {
+  if (dst) COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g_host.stream));
+}
+
+}  // namespace
+}  // namespace cotten
+
+using namespace cotten;
+
+extern "C" {
+
+const char* cotten_version(void) { return "cotten-b200 0.1 (sm_100a)"; }
+const char* cotten_last_error(void) { return g_last_error.c_str(); }
+int cotten_last_launch_count(void) { return g_launches; }
+
+int cotten_fwd(const cotten_desc* desc, const void* q, const void* k, const void* v,
+               const uint8_t* valid, double m, void* out, void* saved_S, void* saved_norms,
+               void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    Layout L = resolve(desc, "cosine_attention_fused");
+    device_fwd(L, q, k, v, valid, m, out, saved_S, saved_norms, (cudaStream_t)stream);
+  });
+}
+
+int cotten_bwd(const cotten_desc* desc, const void* q, const void* k, const void* v,
+               const uint8_t* valid, double m, const void* d_out, const void* saved_S, void* dq,
+               void* dk, void* dv, double* dm_unit, double* dm_total, void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    Layout L = resolve(desc, "cosine_attention_backward");
+    device_bwd(L, q, k, v, valid, m, d_out, saved_S, dq, dk, dv, dm_unit, dm_total,
+               (cudaStream_t)stream);
+  });
+}
+
+int cotten_device_status(int device, int32_t* bits, int reset) {
+  return guarded([&] {
+    if (!bits) usage("cotten_device_status: null output");
+    int prev = 0;
+    COTTEN_CUDA(cudaGetDevice(&prev));
+    COTTEN_CUDA(cudaSetDevice(device));
+    int* w = device_status_word();
+    COTTEN_CUDA(cudaDeviceSynchronize());
+    int h = 0;
+    COTTEN_CUDA(cudaMemcpy(&h, w, sizeof(int), cudaMemcpyDeviceToHost));
+    if (reset) COTTEN_CUDA(cudaMemset(w, 0, sizeof(int)));
+    *bits = h;
+    COTTEN_CUDA(cudaSetDevice(prev));
+  });
+}
+
+int cotten_fwd_host(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                    const uint8_t* valid, double m, void* out, void* saved_S,
+                    void* saved_norms) {
+  g_launches = 0;
+  return guarded([&] {
+    Layout L = resolve(desc, "cosine_attention_fused");
+    if (!q || !k || !v) usage("cosine_attention_fused: null input");
+    host_check_mask(L, valid, "cosine_attention_fused");
+    L.require_dense("cosine_attention_fused");
+    g_host.ensure();
+    const size_t tb = L.span() * elem_size(L.dtype);
+    const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
+    const size_t nbytes = L.units() * 2 * L.N * acc_size(L.dtype);
+    void* dq = h2d(kQ, q, tb);
+    void* dk = h2d(kK, k, tb);
+    void* dv = h2d(kV, v, tb);
+    const uint8_t* dmask =
+        valid ? static_cast<const uint8_t*>(h2d(kMask, valid, (L.B - 1) * L.msb + L.N)) : nullptr;
+    void* dout = out ? g_host.buf(kO, tb) : nullptr;
+    void* dS = saved_S ? g_host.buf(kS, sbytes) : nullptr;
+    void* dN = saved_norms ? g_host.buf(kNorms, nbytes) : nullptr;
+    device_fwd(L, dq, dk, dv, dmask, m, dout, dS, dN, g_host.stream);
+    d2h(out, dout, tb);
+    d2h(saved_S, dS, sbytes);
+    d2h(saved_norms, dN, nbytes);
+    COTTEN_CUDA(cudaStreamSynchronize(g_host.stream));
+  });
+}
+
+int cotten_bwd_host(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                    const uint8_t* valid, double m, const void* d_out, const void* saved_S,
+                    void* dq, void* dk, void* dv, double* dm_unit, double* dm_total) {
+  g_launches = 0;
+  return guarded([&] {
+    Layout L = resolve(desc, "cosine_attention_backward");
+    if (!q || !k || !v || !d_out) usage("cosine_attention_backward: null input");
+    if (!dq || !dk || !dv) usage("cosine_attention_backward: null gradient output");
+    host_check_mask(L, valid, "cosine_attention_backward");
+    L.require_dense("cosine_attention_backward");
+    g_host.ensure();
+    const size_t tb = L.span() * elem_size(L.dtype);
+    const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
+    void* gq = h2d(kQ, q, tb);
+    void* gk = h2d(kK, k, tb);
+    void* gv = h2d(kV, v, tb);
+    void* gdo = h2d(kDO, d_out, tb);
+    const uint8_t* dmask =
+        valid ? static_cast<const uint8_t*>(h2d(kMask, valid, (L.B - 1) * L.msb + L.N)) : nullptr;
+    const void* gS = saved_S ? h2d(kS, saved_S, sbytes) : nullptr;
+    void* gdq = g_host.buf(kDQ, tb);
+    void* gdk = g_host.buf(kDK, tb);
+    void* gdv = g_host.buf(kDV, tb);
+    double* gdm = static_cast<double*>(g_host.buf(kDm, (L.units() + 1) * sizeof(double)));
+    device_bwd(L, gq, gk, gv, dmask, m, gdo, gS, gdq, gdk, gdv, gdm, gdm + L.units(),
+               g_host.stream);
+    d2h(dq, gdq, tb);
+    d2h(dk, gdk, tb);
+    d2h(dv, gdv, tb);
+    d2h(dm_unit, gdm, L.units() * sizeof(double));
+    d2h(dm_total, gdm + L.units(), sizeof(double));
+    COTTEN_CUDA(cudaStreamSynchronize(g_host.stream));
+  });
+}
+
+int cotten_fwd_bwd_host(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                        const uint8_t* valid, double m, const void* d_out, void* out, void* dq,
+                        void* dk, void* dv, double* dm_total) {
+  g_launches = 0;
+  return guarded([&] {
+    Layout L = resolve(desc, "cosine_attention_fused");
+    if (!q || !k || !v || !d_out) usage("cosine_attention_fused: null input");
+    if (!out || !dq || !dk || !dv) usage("cosine_attention_fused: null output");
+    host_check_mask(L, valid, "cosine_attention_fused");
+    L.require_dense("cosine_attention_fused");
+    g_host.ensure();
+    const size_t tb = L.span() * elem_size(L.dtype);
+    const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
+    void* gq = h2d(kQ, q, tb);
+    void* gk = h2d(kK, k, tb);
+    void* gv = h2d(kV, v, tb);
+    void* gdo = h2d(kDO, d_out, tb);
+    const uint8_t* dmask =
+        valid ? static_cast<const uint8_t*>(h2d(kMask, valid, (L.B - 1) * L.msb + L.N)) : nullptr;
+    void* go = g_host.buf(kO, tb);
+    void* gS = g_host.buf(kS, sbytes);
+    void* gdq = g_host.buf(kDQ, tb);
+    void* gdk = g_host.buf(kDK, tb);
+    void* gdv = g_host.buf(kDV, tb);
+    double* gdm = static_cast<double*>(g_host.buf(kDm, (L.units() + 1) * sizeof(double)));
+    device_fwd(L, gq, gk, gv, dmask, m, go, gS, nullptr, g_host.stream);
+    device_bwd(L, gq, gk, gv, dmask, m, gdo, gS, gdq, gdk, gdv, gdm, gdm + L.units(),
+               g_host.stream);
+    d2h(out, go, tb);
+    d2h(dq, gdq, tb);
+    d2h(dk, gdk, tb);
+    d2h(dv, gdv, tb);
+    d2h(dm_total, gdm + L.units(), sizeof(double));
+    COTTEN_CUDA(cudaStreamSynchronize(g_host.stream));
+  });
+}
+
+}  // extern "C"
