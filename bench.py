@@ -235,6 +235,7 @@ def run_ours(args, world, rank, local):
         step(all_marks[s])
     torch.cuda.synchronize()
     barrier(world)
+    gpu_launches = launches[0]
     # keep the GPU busy a little longer so the sampler sees the load
     extra_t0 = time.time()
     while time.time() - extra_t0 < 1.0:
@@ -242,7 +243,6 @@ def run_ours(args, world, rank, local):
         step()
     torch.cuda.synchronize()
     clocks = sampler.stop()
-    gpu_launches = launches[0]
 
     step_ms = [m_[0].elapsed_time(m_[-1]) for m_ in all_marks]
     fwd_ms = [m_[i].elapsed_time(m_[i + 1]) for m_ in all_marks for i in range(layers)]

@@ -23,6 +23,7 @@ struct OpParams {
   void* saved_norms;     // [B*H][2][N] accumulation type or nullptr
   double* dm_unit;       // [B*H] or nullptr
   int* status;           // sticky per-device status word (COTTEN_STATUS_*)
+  void* workspace;       // kernel-specific global scratch (generic bwd: G per unit)
   int64_t B, H, N, D;
   int64_t sb, sh, sn, msb;
   double m, eps;

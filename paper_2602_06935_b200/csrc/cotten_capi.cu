@@ -110,11 +110,12 @@ Layout resolve(const cotten_desc* d, const char* what) {
   return L;
 }
 
-void check_generic_fits(const Layout& L, bool bwd) {
-  const size_t need = L.dtype == COTTEN_F64 ? (bwd ? gen_bwd_smem<double>(L.D) : gen_fwd_smem<double>(L.D))
-                                            : (bwd ? gen_bwd_smem<float>(L.D) : gen_fwd_smem<float>(L.D));
-  if (need > 227 * 1024)
-    usage("cotten: head_dim " + std::to_string(L.D) + " exceeds the shared-memory budget for dtype");
+constexpr size_t kSmemBudget = 227 * 1024;
+
+void check_generic_fits(const Layout& L) {
+  const size_t need = L.dtype == COTTEN_F64 ? gen_fwd_smem<double>(L.D) : gen_fwd_smem<float>(L.D);
+  if (need > kSmemBudget)
+    usage("cotten: head_dim " + std::to_string(L.D) + " exceeds the shared-memory budget");
 }
 
 OpParams make_params(const Layout& L) {
@@ -172,7 +173,7 @@ struct Scratch {
     return ptr;
   }
 };
-thread_local Scratch g_dm_scratch, g_s_scratch;
+thread_local Scratch g_dm_scratch, g_s_scratch, g_g_scratch;
 
 // ---- launches -------------------------------------------------------------
 
@@ -180,9 +181,12 @@ template <typename T>
 void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && fast_fwd_supported<T>(p)) {
-    g_launches += launch_fast_fwd<T>(p, st);
+    const int n = launch_fast_fwd<T>(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fast forward launch failed (tensor map)"};
+    g_launches += n;
   } else {
-    check_generic_fits(L, false);
+    check_generic_fits(L);
     const size_t smem = gen_fwd_smem<A>(L.D);
     COTTEN_CUDA(cudaFuncSetAttribute(cos_fwd_generic<T, A>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -196,13 +200,19 @@ template <typename T>
 void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && fast_bwd_supported<T>(p)) {
-    g_launches += launch_fast_bwd<T>(p, st);
+    const int n = launch_fast_bwd<T>(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fast backward launch failed (tensor map)"};
+    g_launches += n;
   } else {
-    check_generic_fits(L, true);
-    const size_t smem = gen_bwd_smem<A>(L.D);
-    COTTEN_CUDA(cudaFuncSetAttribute(cos_bwd_generic<T, A>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cos_bwd_generic<T, A><<<(unsigned)L.units(), kGenThreads, smem, st>>>(p);
+    const bool gg = gen_bwd_smem<A>(L.D) > kSmemBudget;
+    if (gen_bwd_smem<A>(L.D, gg) > kSmemBudget)
+      usage("cotten: head_dim " + std::to_string(L.D) + " exceeds the shared-memory budget");
+    const size_t smem = gen_bwd_smem<A>(L.D, gg);
+    auto kern = gg ? cos_bwd_generic<T, A, true> : cos_bwd_generic<T, A, false>;
+    if (gg) p.workspace = g_g_scratch.get(L.units() * L.D * L.D * sizeof(A));
+    COTTEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)L.units(), kGenThreads, smem, st>>>(p);
     g_launches += 1;
   }
   COTTEN_CUDA(cudaGetLastError());

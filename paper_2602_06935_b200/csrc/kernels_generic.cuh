@@ -24,10 +24,12 @@ __host__ inline size_t gen_fwd_smem(int64_t D) {
   const int TR = gen_tile_rows<A>(D);
   return sizeof(A) * (D * D + 2 * TR * D + TR);
 }
+// GG: the d x d gradient state G lives in a global workspace instead of
+// shared memory (large head_dim in f64, where S and G do not both fit).
 template <typename A>
-__host__ inline size_t gen_bwd_smem(int64_t D) {
+__host__ inline size_t gen_bwd_smem(int64_t D, bool GG = false) {
   const int TR = gen_tile_rows<A>(D);
-  return sizeof(A) * (2 * D * D + 4 * TR * D + 2 * TR + kGenThreads / 32);
+  return sizeof(A) * ((GG ? 1 : 2) * D * D + 4 * TR * D + 2 * TR + kGenThreads / 32);
 }
 
 template <typename T, typename A>
@@ -152,15 +154,15 @@ __global__ void __launch_bounds__(kGenThreads) cos_fwd_generic(const OpParams p)
 }
 
 // Backward (attention.cpp:397-441) given the saved S.
-template <typename T, typename A>
+template <typename T, typename A, bool GG>
 __global__ void __launch_bounds__(kGenThreads) cos_bwd_generic(const OpParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_cnt;
   const int D = (int)p.D;
   const int TR = gen_tile_rows<A>(D);
   A* S = reinterpret_cast<A*>(smem_raw);
-  A* G = S + D * D;
-  A* t1 = G + D * D;    // Q~ / K~ tile
+  A* G = GG ? static_cast<A*>(p.workspace) + (int64_t)blockIdx.x * D * D : S + D * D;
+  A* t1 = (GG ? S : G) + D * D;  // Q~ / K~ tile
   A* t2 = t1 + TR * D;  // dO / V tile
   A* t3 = t2 + TR * D;  // dQ~ / dK~ tile
   A* t4 = t3 + TR * D;  // dV tile

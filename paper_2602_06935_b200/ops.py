@@ -266,7 +266,7 @@ def forward(q, k, v, valid=None, m=1.0, eps=1e-6, out=None, saved_S=None, saved_
     import torch
     _same_layout(q, k, v, out)
     desc = _tdesc(q, eps, flags, valid)
-    if out is None and saved_S is None and saved_norms is None:
+    if out is None:
         out = torch.empty_like(q)
     check(load().cotten_fwd(ctypes.byref(desc), _tp(q), _tp(k), _tp(v), _tp(valid), float(m),
                             _tp(out), _tp(saved_S), _tp(saved_norms), _stream(stream)))

@@ -22,12 +22,38 @@ def torch_mod():
     return torch
 
 
-def normwise(got, want):
-    """Max over units of max|got-want| / max|want| (units = leading two dims)."""
+def normwise(got, want, scale=None):
+    """Max over units of max|got-want| / max|want| (units = leading two dims).
+    ``scale`` (per unit) raises the denominator to the magnitude of the
+    un-projected gradient for dQ/dK: (g - (g.x~)x~)/n cancels to O(eps) when
+    d_h is 1 or 2, so there max|dQ| says nothing about the rounding budget."""
     g = got.reshape(got.shape[0] * got.shape[1], -1).astype(np.float64)
     w = want.reshape(want.shape[0] * want.shape[1], -1).astype(np.float64)
-    den = np.maximum(np.abs(w).max(1), 1e-30)
+    den = np.abs(w).max(1)
+    if scale is not None:
+        den = np.maximum(den, scale)
+    den = np.maximum(den, 1e-30)
     return float((np.abs(g - w).max(1) / den).max())
+
+
+def proj_scales(inp, valid, m, eps):
+    """Per unit: max_i |s dO_i S^T| / n_q,i and max_valid_i |V_i dA^T| / n_k,i."""
+    B, H, N, D = inp["q"].shape
+    sq, sk = np.zeros(B * H), np.zeros(B * H)
+    for b in range(B):
+        vm = None if valid is None else valid[b]
+        for hh in range(H):
+            r = oracle.fwd(inp["q"][b, hh], inp["k"][b, hh], inp["v"][b, hh], vm, m, eps)
+            tn = N if vm is None else int(vm.sum())
+            s = np.exp(-m * np.log(tn))
+            g = s * inp["d_out"][b, hh] @ r["S"].T
+            sq[b * H + hh] = np.abs(g / r["norm_q"][:, None]).max()
+            dA = s * r["qn"].T @ inp["d_out"][b, hh]
+            gk = inp["v"][b, hh] @ dA.T / r["norm_k"][:, None]
+            if vm is not None:
+                gk = gk[vm != 0]
+            sk[b * H + hh] = np.abs(gk).max()
+    return sq, sk
 
 
 def run_gpu(h, valid, m, eps, dtype="f32", flags=0, layout="bhnd"):
@@ -81,11 +107,14 @@ def oracle_f64(inp, valid, m, eps):
     return (*outs, dm)
 
 
-def assert_parity(res, ref, valid, dtype):
+def assert_parity(res, ref, valid, dtype, m=None, eps=None):
     tol = TOL[dtype]
     out, dq, dk, dv, dm = ref
+    scales = {}
+    if m is not None and res["inputs"]["q"].shape[-1] <= 2:
+        scales["dq"], scales["dk"] = proj_scales(res["inputs"], valid, m, eps)
     for name, want in (("out", out), ("dq", dq), ("dk", dk), ("dv", dv)):
-        err = normwise(res[name], want)
+        err = normwise(res[name], want, scales.get(name))
         assert err <= tol, f"{name}: normwise {err:.3e} > {tol}"
     # dm per unit, normwise over the batch of units (a sum of d^2 products can
     # cancel, so a per-unit relative error is not meaningful near zero)
@@ -126,7 +155,7 @@ def test_head_dims_f32(D):
     h = inputs.make_host(B, H, N, D, seed=D)
     valid = inputs.random_mask(B, N, D)
     res = run_gpu(h, valid, 1.25, 1e-6, "f32")
-    assert_parity(res, oracle_for(res["inputs"], valid, 1.25, 1e-6), valid, "f32")
+    assert_parity(res, oracle_for(res["inputs"], valid, 1.25, 1e-6), valid, "f32", 1.25, 1e-6)
 
 
 @pytest.mark.parametrize("D", [1, 4, 16, 32, 64])
@@ -136,7 +165,7 @@ def test_f64_matches_oracle_tightly(D):
     h = {n: rng.uniform(-2, 2, (B, H, N, D)) for n in ("q", "k", "v", "d_out")}
     valid = inputs.random_mask(B, N, 100 + D)
     res = run_gpu(h, valid, 0.6, 1e-9, "f64")
-    assert_parity(res, oracle_f64(res["inputs"], valid, 0.6, 1e-9), valid, "f64")
+    assert_parity(res, oracle_f64(res["inputs"], valid, 0.6, 1e-9), valid, "f64", 0.6, 1e-9)
 
 
 @pytest.mark.parametrize("D", [32, 64])
