@@ -49,8 +49,16 @@ struct ScaleTable {
   double coef[kMaxN + 1];
 };
 
+// A slot holds round8(N) rows (rows [N, round8(N)) are kept zero so row
+// reductions run whole 8-row groups), rounded up to the 1 KB alignment of the
+// 128B swizzle.  Row-outputs of a last 32-row block may read up to 31 rows
+// past it (into the next slot or the matrices after the ring); those rows
+// only feed outputs that are never stored.
 __host__ __device__ constexpr uint32_t tile_bytes(int N) {
-  return (uint32_t)((N + 31) / 32) * 32u * kRowBytes;  // whole 32-row blocks, 4 KB multiple
+  // >= 4 KB: a slot must also hold one warp's 32x32 partial sums
+  return (((uint32_t)(N + 7) / 8u * 8u * kRowBytes) + 1023u) / 1024u * 1024u < 4096u
+             ? 4096u
+             : (((uint32_t)(N + 7) / 8u * 8u * kRowBytes) + 1023u) / 1024u * 1024u;
 }
 
 // ---- PTX wrappers ---------------------------------------------------------
@@ -73,15 +81,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps until the phase
+// completes instead of spinning on issue slots the co-resident CTA needs.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
@@ -291,7 +301,7 @@ struct Plan {
     ns = NS;
     off_ring = 0;
     off_mat = off_ring + (uint32_t)NS * tb;
-    off_inv = off_mat + (bwd ? 3 * 4096 : 4096);
+    off_inv = off_mat + (bwd ? 2 * 4096 : 4096);  // bwd: [S^T | dA^T] overlay, then dA
     off_flag = off_inv + (bwd ? 2 * kMaxN * 4 : 0);
     off_misc = off_flag + kMaxN;  // per-warp counts (8 ints), then dm partials (8 doubles)
     off_bar = off_misc + 32 + 8 * 8;
@@ -310,28 +320,44 @@ struct RingPos {
   }
 };
 
-// Zero rows [N, round32(N)) of every slot once, so row-reductions may run
+// Zero rows [N, round8(N)) of every slot once, so row-reductions may run
 // whole 8-row groups and row-outputs never read uninitialised memory.
+__host__ __device__ constexpr uint32_t tail_end(int N) { return (uint32_t)(N + 7) / 8u * 8u * kRowBytes; }
+
 __device__ __forceinline__ void zero_tails(uint8_t* ring, const Plan& pl, int N, int tid,
                                            int nthreads) {
   const uint32_t lo = (uint32_t)N * kRowBytes;
-  const uint32_t per = (pl.tb - lo) / 16;
+  const uint32_t per = (tail_end(N) - lo) / 16;
   for (uint32_t i = tid; i < per * (uint32_t)pl.ns; i += nthreads) {
     const uint32_t s = i / per, k = i - s * per;
     st4(ring + s * pl.tb + lo + 16 * k, make_float4(0.f, 0.f, 0.f, 0.f));
   }
 }
 
-// Consumer-side: valid flags for sequence b into flag[], returns true_n.
-template <int NW>
-__device__ __forceinline__ int load_flags(const OpParams& p, int64_t b, int N, uint8_t* flag,
-                                          int* cnt, int tid) {
-  const uint8_t* vrow = p.valid ? p.valid + b * p.msb : nullptr;
-  int f = 0;
-  if (tid < N) {  // NW*32 >= N
-    f = vrow == nullptr || vrow[tid] != 0;
-    flag[tid] = (uint8_t)f;
+// Consumer-side, one unit ahead: the valid flag of row tid of unit u's
+// sequence (registers; consumed by publish_flags at the next unit).
+__device__ __forceinline__ int fetch_flag(const OpParams& p, int u, int units, int tid) {
+  if (u >= units || tid >= (int)p.N) return 0;
+  if (p.valid == nullptr) return 1;
+  const int64_t b = u / (int)p.H;
+  return __ldg(p.valid + b * p.msb + tid) != 0;
+}
+// Saved S of unit u (backward), one unit ahead: element pairs (a, c4..c4+3).
+template <int PERS, int NW>
+__device__ __forceinline__ void fetch_S(const OpParams& p, int u, int units, int tid,
+                                        float4 (&sr)[PERS]) {
+  if (u >= units) return;
+  const float* gS = static_cast<const float*>(p.saved_S) + (int64_t)u * 1024;
+#pragma unroll
+  for (int k = 0; k < PERS; ++k) {
+    const int i = tid + k * NW * 32;
+    if (i < 256) sr[k] = __ldg(reinterpret_cast<const float4*>(gS + (i & 31) * 32 + (i >> 5) * 4));
   }
+}
+// Valid flags into flag[] and true_n (attention.cpp:26-33); one consumer sync.
+template <int NW>
+__device__ __forceinline__ int publish_flags(int f, int N, uint8_t* flag, int* cnt, int tid) {
+  if (tid < N) flag[tid] = (uint8_t)f;  // NW*32 >= N
   const unsigned m = __ballot_sync(0xffffffffu, f);
   if ((tid & 31) == 0) cnt[tid >> 5] = __popc(m);
   consumer_sync<NW>();
@@ -401,8 +427,11 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_fwd_d32_kernel(
   const int rg = lane >> 2, cg = lane & 3;
   float* gS_all = static_cast<float*>(p.saved_S);
   RingPos pos;
+  int fnext = fetch_flag(p, blockIdx.x, units, tid);
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int b = u / H, h = u - b * H;
+    const int fcur = fnext;
+    fnext = fetch_flag(p, u + gridDim.x, units, tid);  // hidden behind this unit
     const int sk = pos.slot;
     const uint32_t phk = pos.phase;
     pos.next(NS);
@@ -418,7 +447,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_fwd_d32_kernel(
     }
     uint8_t* Kt = ring + sk * pl.tb;
     uint8_t* Vt = ring + sv * pl.tb;
-    const int true_n = load_flags<NW>(p, b, N, flag, cnt, tid);
+    const int true_n = publish_flags<NW>(fcur, N, flag, cnt, tid);
     const int64_t base = (int64_t)b * p.sb + (int64_t)h * p.sh;
     float* norms = norms_all ? norms_all + (int64_t)u * 2 * N : nullptr;
     if (true_n == 0) {  // UsageError in the reference (attention.cpp:44): NaN outputs
@@ -469,7 +498,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_fwd_d32_kernel(
     }
     if (N * kRowBytes < (uint32_t)((NW + 1) / 2) * 4096u) {  // partials spilled into tails
       consumer_sync<NW>();
-      for (int i = tid; i < (int)((pl.tb - N * kRowBytes) / 16); i += NW * 32) {
+      for (int i = tid; i < (int)((tail_end(N) - N * kRowBytes) / 16); i += NW * 32) {
         st4(Kt + N * kRowBytes + 16 * i, make_float4(0.f, 0.f, 0.f, 0.f));
         st4(Vt + N * kRowBytes + 16 * i, make_float4(0.f, 0.f, 0.f, 0.f));
       }
@@ -527,7 +556,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
   uint8_t* ring = smem + pl.off_ring;
   float* St = reinterpret_cast<float*>(smem + pl.off_mat);
   float* dA = St + 1024;
-  float* dAt = dA + 1024;
+  float* dAt = St;  // S^T is dead once <G,S> is taken; dA^T reuses it
   float* inv_q = reinterpret_cast<float*>(smem + pl.off_inv);
   float* inv_k = inv_q + kMaxN;
   uint8_t* flag = smem + pl.off_flag;
@@ -578,8 +607,27 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
   float* dK = static_cast<float*>(p.dk);
   float* dV = static_cast<float*>(p.dv);
   RingPos pos;
+  constexpr int PERS = (256 + NW * 32 - 1) / (NW * 32);
+  float4 snext[PERS];
+  fetch_S<PERS, NW>(p, blockIdx.x, units, tid, snext);
+  int fnext = fetch_flag(p, blockIdx.x, units, tid);
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int b = u / H, h = u - b * H;
+    // S^T from the prefetched saved state: St[c][a] = S[a][c] (a = lane: conflict-free)
+#pragma unroll
+    for (int k = 0; k < PERS; ++k) {
+      const int i = tid + k * NW * 32;
+      if (i < 256) {
+        const int a = i & 31, c4 = (i >> 5) * 4;
+        St[(c4 + 0) * 32 + a] = snext[k].x;
+        St[(c4 + 1) * 32 + a] = snext[k].y;
+        St[(c4 + 2) * 32 + a] = snext[k].z;
+        St[(c4 + 3) * 32 + a] = snext[k].w;
+      }
+    }
+    const int fcur = fnext;
+    fetch_S<PERS, NW>(p, u + gridDim.x, units, tid, snext);  // next unit, hidden behind this one
+    fnext = fetch_flag(p, u + gridDim.x, units, tid);
     int sl[4];
     uint32_t ph[4];
     for (int t = 0; t < 4; ++t) {
@@ -591,19 +639,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
     uint8_t* Gt = ring + sl[1] * pl.tb;  // dO
     uint8_t* Kt = ring + sl[2] * pl.tb;
     uint8_t* Vt = ring + sl[3] * pl.tb;
-    // S^T from the saved state: St[c][a] = S[a][c] (conflict-free: a = lane)
-    {
-      const float* gS = static_cast<const float*>(p.saved_S) + (int64_t)u * 1024;
-      for (int i = tid; i < 256; i += NW * 32) {
-        const int a = i & 31, c4 = (i >> 5) * 4;
-        const float4 s = *reinterpret_cast<const float4*>(gS + a * 32 + c4);
-        St[(c4 + 0) * 32 + a] = s.x;
-        St[(c4 + 1) * 32 + a] = s.y;
-        St[(c4 + 2) * 32 + a] = s.z;
-        St[(c4 + 3) * 32 + a] = s.w;
-      }
-    }
-    const int true_n = load_flags<NW>(p, b, N, flag, cnt, tid);  // includes a consumer sync
+    const int true_n = publish_flags<NW>(fcur, N, flag, cnt, tid);  // includes a consumer sync
     const int64_t base = (int64_t)b * p.sb + (int64_t)h * p.sh;
     if (true_n == 0) {
       if (tid == 0) {
@@ -680,6 +716,16 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
           d = fmaf(g4[k].z, St[(c + 2) * 32 + a], d);
           d = fmaf(g4[k].w, St[(c + 3) * 32 + a], d);
           dot += (double)d;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      consumer_sync<NW>();  // partials and S^T read: both regions may now be overwritten
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e4 = tid + k * NW * 32;
+        if (e4 < 256) {
+          const int a = e4 >> 3, c = (e4 & 7) * 4;
           const float4 s = make_float4(g4[k].x * scale, g4[k].y * scale, g4[k].z * scale,
                                        g4[k].w * scale);  // dA = s G (:412-413)
           reinterpret_cast<float4*>(dA)[e4] = s;
@@ -689,15 +735,11 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
           dAt[(c + 3) * 32 + a] = s.w;
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (N * kRowBytes < (uint32_t)((NW + 1) / 2) * 4096u) {  // partials spilled into tails
-        consumer_sync<NW>();
-        for (int i = tid; i < (int)((pl.tb - N * kRowBytes) / 16); i += NW * 32) {
+      if (N * kRowBytes < (uint32_t)((NW + 1) / 2) * 4096u)  // partials spilled into tails
+        for (int i = tid; i < (int)((tail_end(N) - N * kRowBytes) / 16); i += NW * 32) {
           st4(Qt + N * kRowBytes + 16 * i, make_float4(0.f, 0.f, 0.f, 0.f));
           st4(Gt + N * kRowBytes + 16 * i, make_float4(0.f, 0.f, 0.f, 0.f));
         }
-      }
       consumer_sync<NW>();  // dA complete; Q, dO slots free
       if (lane == 0) red[warp] = dot;
       if (tid == 0) {
@@ -909,8 +951,9 @@ inline cudaError_t bwd_nw(const CUtensorMap& q, const CUtensorMap& k, const CUte
                           const CUtensorMap& g, const OpParams& p, const d32::ScaleTable& tab,
                           cudaStream_t st) {
   const int N = (int)p.N;
-  // two CTAs per SM when 8 slots fit in half the SM, else one CTA with 8 slots
-  const uint32_t budget = d32::Plan(N, 8, true).bytes <= 113 * 1024 ? 113 * 1024 : 227 * 1024;
+  // two (or more) CTAs per SM when a whole unit's 4 tiles fit in half the SM,
+  // else one CTA with up to 8 slots
+  const uint32_t budget = d32::Plan(N, 4, true).bytes <= 113 * 1024 ? 113 * 1024 : 227 * 1024;
   const int ns = pick_slots(N, true, budget, 4, 8);
   switch (ns) {
     case 4: return bwd_nw_ns<NW, 4>(q, k, v, g, p, tab, st);
