@@ -1,31 +1,30 @@
-// Fast fp32 cosine-attention kernels for head_dim 32 — the ML-1M / ML-20M /
-// Beauty shapes (model d = 64 over 2 heads) — and seq_len <= 1024.
+// Fast fp32 cosine-attention kernels for head_dim 32 (the ML-1M / ML-20M /
+// Beauty shapes: model d = 64 over 2 heads) and seq_len <= 256.
 //
-// Design: warp per unit.  Every warp of a persistent CTA owns whole
-// (sequence, head) units (unit = warp_id + k * total_warps) and streams their
-// 32-row tiles (cp.async.bulk.tensor, 128-byte swizzle, 4 KB per tensor per
-// chunk; rows past N are zero-filled by the TMA bounds check) through its own
-// NSTG-deep ring of shared-memory stages, each guarded by one mbarrier.  Lane
-// 0 re-arms a stage the moment the warp has consumed it, so NSTG-1 chunks are
-// always in flight.  No CTA barrier, no cross-warp reduction: the 32x32 state
-// (S in the forward, G in the backward) accumulates in the warp's registers in
-// row order, so results are deterministic and warps never wait on each other.
-//
-// Per 32-row chunk the warp
-//   * normalises rows in place (8 lanes per row, shuffle-reduced norms),
-//   * accumulates a row-reduction  R += x_i^T y_i   (S = K~^T V, G = Q~^T dO):
-//     lane (ag, bg) holds R[8ag..8ag+8][4bg..4bg+4] as 16 float2 registers
-//     updated with FFMA2 (packed fp32 FMA, scalar operand broadcast):
-//     16 FFMA2 per row for 3 LDS.128,
-//   * or a row-output  o_i = x_i M  (O = Q S, dQ~ = dO S^T, dV = K~ dA,
-//     dK~ = V dA^T): lane (rg, cg) holds rows rg+8j (j<4) x columns
-//     {4cg..4cg+3, 16+4cg..16+4cg+3}, 16 FFMA2 per contraction step for
-//     3 LDS.128; the 128-byte swizzle puts the 8 row groups on 8 bank groups.
-// Nothing but the outputs and the 4 KB state S per unit reaches HBM: no Q~,
-// K~ or N x N buffer exists.  Mask semantics follow attention.cpp exactly:
-// padded K rows are selected to zero (never read), dK / dV rows of padded
-// positions are exact zeros, Q and dQ cover every row, and s = exp(-m ln n)
-// comes from fp64 (a host table for n <= 256, fp64 in-kernel above).
+// Persistent, warp-specialised CTAs (a few per SM, sized from the shared-
+// memory budget).  One producer warp streams each unit's N x 32 tiles
+// (cp.async.bulk.tensor, 128-byte swizzle) into a ring of NS shared-memory
+// slots guarded by full/empty mbarriers, in the order the consumers need
+// them — forward: K, V, Q; backward: Q, dO, K, V — so the next unit's tiles
+// land while the current one is computed.  NW = ceil(N/32) consumer warps;
+// warp w owns rows [32w, 32w+32) of every tile.  Per row block it
+//   * normalises its rows in place (8 lanes per row, shuffle-reduced norms),
+//   * accumulates a 32x32 row-reduction  R += x_i^T y_i   (S = K~^T V,
+//     G = Q~^T dO): lane (ag, bg) holds R[8ag..8ag+8][4bg..4bg+4] as 16
+//     float2 accumulators updated with FFMA2 (packed fp32 FMA with one
+//     scalar operand broadcast) — 16 FFMA2 per row for 3 LDS.128,
+//   * or emits a row-output  o_i = x_i M  (O = Q S, dQ~ = dO S^T,
+//     dV = K~ dA, dK~ = V dA^T): lane (rg, cg) holds rows rg+8j (j<4) x
+//     columns {4cg..4cg+3, 16+4cg..16+4cg+3}, again 16 FFMA2 per contraction
+//     step for 3 LDS.128; the 128-byte swizzle puts the 8 row groups on 8
+//     distinct bank groups.
+// All swizzled addresses are per-lane base registers plus immediates.  Per-
+// warp partial reductions are summed through shared memory in a fixed order
+// (deterministic), overlaying the tiles they were computed from.  Nothing
+// but the outputs and the 4 KB state S reaches HBM: no Q~, K~ or N x N.
+// Mask semantics follow attention.cpp exactly: padded K rows are selected to
+// zero (never read), dK / dV rows of padded positions are exact zeros, Q and
+// dQ cover every row, s = exp(-m ln true_n) is computed in fp64 on the host.
 #pragma once
 #include <cuda.h>
 
@@ -41,23 +40,25 @@ namespace d32 {
 
 constexpr int kD = 32;
 constexpr uint32_t kRowBytes = 128;
-constexpr uint32_t kTile = 32 * kRowBytes;  // one 32-row chunk of one tensor
-constexpr int kMaxN = 1024;                 // flag words / prefetch registers
-constexpr int kTabN = 256;                  // host-computed scale table range
+constexpr int kMaxN = 256;
 
-// s[n] = exp(-m ln n) (attention.cpp:303-304, :402-403) and
-// coef[n] = -ln(n) * s[n] (:408), in fp64 on the host; entry 0 is NaN (the
-// reference's UsageError for a sequence without real rows).
+// Per-call constants the host computes in fp64 exactly as attention.cpp:
+// s[n] = exp(-m ln n) (:303-304, :402-403), coef[n] = -ln(n) * s[n] (:408).
 struct ScaleTable {
-  float s[kTabN + 1];
-  double coef[kTabN + 1];
+  float s[kMaxN + 1];
+  double coef[kMaxN + 1];
 };
 
-__device__ __forceinline__ float scale_of(const ScaleTable& t, int n, double m) {
-  return n <= kTabN ? t.s[n] : (float)exp(-m * log((double)n));
-}
-__device__ __forceinline__ double coef_of(const ScaleTable& t, int n, double m) {
-  return n <= kTabN ? t.coef[n] : -log((double)n) * (double)(float)exp(-m * log((double)n));
+// A slot holds round8(N) rows (rows [N, round8(N)) are kept zero so row
+// reductions run whole 8-row groups), rounded up to the 1 KB alignment of the
+// 128B swizzle.  Row-outputs of a last 32-row block may read up to 31 rows
+// past it (into the next slot or the matrices after the ring); those rows
+// only feed outputs that are never stored.
+__host__ __device__ constexpr uint32_t tile_bytes(int N) {
+  // >= 4 KB: a slot must also hold one warp's 32x32 partial sums
+  return (((uint32_t)(N + 7) / 8u * 8u * kRowBytes) + 1023u) / 1024u * 1024u < 4096u
+             ? 4096u
+             : (((uint32_t)(N + 7) / 8u * 8u * kRowBytes) + 1023u) / 1024u * 1024u;
 }
 
 // ---- PTX wrappers ---------------------------------------------------------
@@ -70,10 +71,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// Order this thread's (and, after __syncwarp, the warp's) generic-proxy reads
-// of a stage before the async-proxy TMA write that refills it.
-__device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -81,8 +78,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // try_wait with a suspend-time hint: a waiting warp sleeps until the phase
-// completes instead of spinning on issue slots its neighbours need.
+// completes instead of spinning on issue slots the co-resident CTA needs.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -106,6 +106,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+// Named barrier 1 over the consumer warps only (the producer never joins).
+template <int NW>
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+}
 
 __device__ __forceinline__ float4 ld4(const uint8_t* p) {
   return *reinterpret_cast<const float4*>(p);
@@ -119,20 +124,20 @@ __device__ __forceinline__ float sel4(const float4& v, int i) {
   return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
-// ---- chunk-level building blocks (one warp, one 128B-swizzled 32-row tile) --
+// ---- building blocks (warp-level; X, Y are 128B-swizzled tiles) ------------
 
-// In place: x <- valid ? x / sqrt(|x|^2 + eps) : 0 for rows [0, rows) of the
-// tile (attention.cpp:83-87, :334-342, :366-372); valid = bit r of vword.
-// inv[r] <- valid ? 1/sqrt(..) : 0, norm_out[r] <- valid ? sqrt(..) : 1 (:336).
-__device__ __forceinline__ void normalize_tile(uint8_t* X, int rows, uint32_t vword, float eps,
-                                               float* inv, float* norm_out, int lane) {
+// In place: x <- valid ? x / sqrt(|x|^2 + eps) : 0 for rows [r0, r0+32) ∩ [0, N)
+// (attention.cpp:83-87, :334-342, :366-372); inv[r] <- 1/sqrt(..) (0 if padded).
+__device__ __forceinline__ void normalize_rows(uint8_t* X, int r0, int N, const uint8_t* flag,
+                                               float eps, float* inv, float* norm_out,
+                                               int lane) {
   const int sub = lane >> 3, c = lane & 7;
-  uint8_t* be = X + sub * kRowBytes + ((c ^ sub) << 4);        // rows with (r & 7) == sub
-  uint8_t* bo = X + sub * kRowBytes + ((c ^ (sub + 4)) << 4);  // rows with (r & 7) == sub + 4
+  uint8_t* be = X + (r0 + sub) * kRowBytes + ((c ^ sub) << 4);        // rows with (r&7) = sub
+  uint8_t* bo = X + (r0 + sub) * kRowBytes + ((c ^ (sub + 4)) << 4);  // rows with (r&7) = sub+4
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
-    if (4 * g >= rows) break;  // warp-uniform
-    const int r = 4 * g + sub;
+    const int r = r0 + 4 * g + sub;
+    if (r0 + 4 * g >= N) break;  // warp-uniform
     uint8_t* a = (g & 1 ? bo : be) + 512 * g;
     float4 x = ld4(a);
     float ss = x.x * x.x;
@@ -142,8 +147,8 @@ __device__ __forceinline__ void normalize_tile(uint8_t* X, int rows, uint32_t vw
     ss += __shfl_xor_sync(0xffffffffu, ss, 1);
     ss += __shfl_xor_sync(0xffffffffu, ss, 2);
     ss += __shfl_xor_sync(0xffffffffu, ss, 4);
-    if (r < rows) {
-      const bool valid = (vword >> r) & 1u;
+    if (r < N) {
+      const bool valid = flag == nullptr || flag[r] != 0;
       const float nrm = sqrtf(ss + eps);
       const float iv = 1.0f / nrm;
       x = valid ? make_float4(x.x * iv, x.y * iv, x.z * iv, x.w * iv)
@@ -151,26 +156,28 @@ __device__ __forceinline__ void normalize_tile(uint8_t* X, int rows, uint32_t vw
       st4(a, x);
       if (c == 0) {
         if (inv != nullptr) inv[r] = valid ? iv : 0.f;
-        if (norm_out != nullptr) norm_out[r] = valid ? nrm : 1.0f;
+        if (norm_out != nullptr) norm_out[r] = valid ? nrm : 1.0f;  // :336, :343
       }
     }
   }
 }
 
-// acc[y][p] += x[8ag+2p .. +1] * y[4bg+y] over rows [0, round8(rows)) of the
-// tiles; rows >= N were zero-filled by the TMA and padded K rows zeroed.
-__device__ __forceinline__ void row_reduce_tile(const uint8_t* X, const uint8_t* Y, int rows,
-                                                float2 (&acc)[4][4], int lane) {
+// acc[y][p] += x[8ag+2p .. +1] * y[4bg+y] for rows [r0, min(r0+32, round8(N))).
+// Rows in [N, round32(N)) of every slot are zero (see zero_tails).
+__device__ __forceinline__ void row_reduce(const uint8_t* X, const uint8_t* Y, int r0, int N,
+                                           float2 (&acc)[4][4], int lane) {
   const int ag = lane >> 3, bg = lane & 7;
+  const uint8_t* xb = X + r0 * kRowBytes;
+  const uint8_t* yb = Y + r0 * kRowBytes;
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
-    if (8 * t >= rows) break;  // warp-uniform
+    if (r0 + 8 * t >= N) break;  // warp-uniform
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
-      const int r = 8 * t + s;
-      const float4 x0 = ld4(X + r * kRowBytes + (((2 * ag) ^ s) << 4));
-      const float4 x1 = ld4(X + r * kRowBytes + (((2 * ag + 1) ^ s) << 4));
-      const float4 y = ld4(Y + r * kRowBytes + ((bg ^ s) << 4));
+      const int rr = 8 * t + s;
+      const float4 x0 = ld4(xb + rr * kRowBytes + (((2 * ag) ^ s) << 4));
+      const float4 x1 = ld4(xb + rr * kRowBytes + (((2 * ag + 1) ^ s) << 4));
+      const float4 y = ld4(yb + rr * kRowBytes + ((bg ^ s) << 4));
       const float2 xp[4] = {f2(x0.x, x0.y), f2(x0.z, x0.w), f2(x1.x, x1.y), f2(x1.z, x1.w)};
 #pragma unroll
       for (int yy = 0; yy < 4; ++yy)
@@ -180,47 +187,34 @@ __device__ __forceinline__ void row_reduce_tile(const uint8_t* X, const uint8_t*
   }
 }
 
-// Row-reduction registers -> row-major 32x32 matrix (optionally scaled).
-__device__ __forceinline__ void store_rowmajor(float* M, const float2 (&acc)[4][4], float sc,
-                                               int lane) {
+// Store a warp's 32x32 partial (row-reduction layout) to part[a*32 + b].
+__device__ __forceinline__ void store_partial(float* part, const float2 (&acc)[4][4], int lane) {
   const int ag = lane >> 3, bg = lane & 7;
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const int a = 8 * ag + 2 * p;
-    *reinterpret_cast<float4*>(M + a * 32 + 4 * bg) = make_float4(
-        acc[0][p].x * sc, acc[1][p].x * sc, acc[2][p].x * sc, acc[3][p].x * sc);
-    *reinterpret_cast<float4*>(M + (a + 1) * 32 + 4 * bg) = make_float4(
-        acc[0][p].y * sc, acc[1][p].y * sc, acc[2][p].y * sc, acc[3][p].y * sc);
-  }
-}
-// ... and its transpose (M^T[b][a] = R[a][b]): row b = 4bg+y, columns 8ag..8ag+7.
-__device__ __forceinline__ void store_transposed(float* Mt, const float2 (&acc)[4][4], float sc,
-                                                 int lane) {
-  const int ag = lane >> 3, bg = lane & 7;
-#pragma unroll
-  for (int y = 0; y < 4; ++y) {
-    float* row = Mt + (4 * bg + y) * 32 + 8 * ag;
-    *reinterpret_cast<float4*>(row) = make_float4(acc[y][0].x * sc, acc[y][0].y * sc,
-                                                  acc[y][1].x * sc, acc[y][1].y * sc);
-    *reinterpret_cast<float4*>(row + 4) = make_float4(acc[y][2].x * sc, acc[y][2].y * sc,
-                                                      acc[y][3].x * sc, acc[y][3].y * sc);
+    *reinterpret_cast<float4*>(part + a * 32 + 4 * bg) =
+        make_float4(acc[0][p].x, acc[1][p].x, acc[2][p].x, acc[3][p].x);
+    *reinterpret_cast<float4*>(part + (a + 1) * 32 + 4 * bg) =
+        make_float4(acc[0][p].y, acc[1][p].y, acc[2][p].y, acc[3][p].y);
   }
 }
 
-// o[j][.] (tile row rg+8j; columns chunk cg then chunk cg+4) = x_row . M, M a
-// plain row-major 32x32 fp32 matrix in shared memory (broadcast reads).
-__device__ __forceinline__ void row_output_tile(const uint8_t* X, const float* M,
-                                                float2 (&o)[4][4], int lane) {
+// o[j][.] (row r0+rg+8j, columns chunk cg then chunk cg+4) = x_row . M with M
+// a plain row-major 32x32 fp32 matrix in shared memory.  Rows >= N produce
+// values that are never stored.
+__device__ __forceinline__ void row_output(const uint8_t* X, const float* M, int r0,
+                                           float2 (&o)[4][4], int lane) {
   const int rg = lane >> 2, cg = lane & 3;
 #pragma unroll
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int p = 0; p < 4; ++p) o[j][p] = f2(0.f, 0.f);
-  const uint8_t* xb = X + rg * kRowBytes;
+  const uint8_t* xb = X + (r0 + rg) * kRowBytes;
   const float* mb = M + 4 * cg;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const uint8_t* xc = xb + ((c ^ rg) << 4);  // (r & 7) == rg for the four rows
+    const uint8_t* xc = xb + ((c ^ rg) << 4);  // (r & 7) == rg for all four rows
     float4 xv[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) xv[j] = ld4(xc + 1024 * j);
@@ -238,10 +232,11 @@ __device__ __forceinline__ void row_output_tile(const uint8_t* X, const float* M
   }
 }
 
-// The 8 values of tile row rg+8j that lane (rg, cg) owns in a row-output.
-__device__ __forceinline__ void own_cols(const uint8_t* X, int j, int lane, float (&v)[8]) {
+// The 8 values of row r0+rg+8j that lane (rg, cg) owns in a row-output.
+__device__ __forceinline__ void own_cols(const uint8_t* X, int r0, int j, int lane,
+                                         float (&v)[8]) {
   const int rg = lane >> 2, cg = lane & 3;
-  const uint8_t* xb = X + (rg + 8 * j) * kRowBytes;
+  const uint8_t* xb = X + (r0 + rg + 8 * j) * kRowBytes;
   const float4 a = ld4(xb + ((cg ^ rg) << 4)), b = ld4(xb + (((cg + 4) ^ rg) << 4));
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
   v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
@@ -257,323 +252,430 @@ __device__ __forceinline__ void store_row(float* dst, int cg, const float (&v)[8
   *reinterpret_cast<float4*>(dst + 4 * cg) = make_float4(v[0], v[1], v[2], v[3]);
   *reinterpret_cast<float4*>(dst + 16 + 4 * cg) = make_float4(v[4], v[5], v[6], v[7]);
 }
-__device__ __forceinline__ float row_sum4(float x) {  // over the 4 lanes sharing a row
+__device__ __forceinline__ float row_sum4(float x) {  // over the 4 lanes of a row
   x += __shfl_xor_sync(0xffffffffu, x, 1);
   x += __shfl_xor_sync(0xffffffffu, x, 2);
   return x;
 }
 
-// ---- per-warp shared-memory plan ------------------------------------------
-
-template <bool BWD, int NSTG>
-struct WarpPlan {
-  static constexpr uint32_t kStage = 2 * kTile;  // two tensors per chunk
-  static constexpr uint32_t off_mat = NSTG * kStage;
-  static constexpr uint32_t off_mat2 = off_mat + 4096;  // bwd: dA (mat 1 holds S^T, then dA^T)
-  static constexpr uint32_t off_inv = off_mat + (BWD ? 8192 : 4096);
-  static constexpr uint32_t off_flag = off_inv + (BWD ? 128 : 0);
-  static constexpr uint32_t off_bar = off_flag + 4 * (kMaxN / 32);
-  static constexpr uint32_t bytes = (off_bar + 8 * NSTG + 1023) / 1024 * 1024;
-};
-
-// The valid-flag bytes of unit u's sequence for rows lane + 32k (k < nc),
-// packed four per register: fetched one unit ahead.
-__device__ __forceinline__ void fetch_flags(const OpParams& p, int u, int units, int nc, int lane,
-                                            uint32_t (&fr)[kMaxN / 128]) {
+// Sum the NW per-warp partials (spread over two tiles: warps < half in A,
+// the rest in B) into dst[e] in a fixed order; returns the per-thread
+// float4s in out4 (PER of them).
+template <int NW, int PER>
+__device__ __forceinline__ void reduce_partials(const float* A, const float* B, int tid,
+                                                float4 (&out4)[PER]) {
+  constexpr int HALF = (NW + 1) / 2;
 #pragma unroll
-  for (int i = 0; i < kMaxN / 128; ++i) fr[i] = 0;
-  if (u >= units) return;
-  if (p.valid == nullptr) {
+  for (int k = 0; k < PER; ++k) {
+    const int e4 = tid + k * NW * 32;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e4 < 256) {
 #pragma unroll
-    for (int i = 0; i < kMaxN / 128; ++i) fr[i] = 0x01010101u;
-    return;
-  }
-  const uint8_t* row = p.valid + (int64_t)(u / (int)p.H) * p.msb;
-  const int N = (int)p.N;
-#pragma unroll
-  for (int k = 0; k < kMaxN / 32; ++k) {
-    if (k >= nc) break;
-    const int r = lane + 32 * k;
-    const uint32_t f = r < N ? (uint32_t)(__ldg(row + r) != 0) : 0u;
-    fr[k >> 2] |= f << (8 * (k & 3));
+      for (int w = 0; w < NW; ++w) {
+        const float* src = (w < HALF ? A + w * 1024 : B + (w - HALF) * 1024);
+        const float4 t = reinterpret_cast<const float4*>(src)[e4];
+        s.x += t.x;
+        s.y += t.y;
+        s.z += t.z;
+        s.w += t.w;
+      }
+    }
+    out4[k] = s;
   }
 }
-// Flag words (bit l of word k = row 32k+l valid) into shared memory; true_n.
-__device__ __forceinline__ int publish_flags(const uint32_t (&fr)[kMaxN / 128], int nc,
-                                             uint32_t* flagw, int lane) {
+template <int NW>
+__device__ __forceinline__ float* partial_slot(uint8_t* A, uint8_t* B, int warp) {
+  constexpr int HALF = (NW + 1) / 2;
+  return reinterpret_cast<float*>(warp < HALF ? A + warp * 4096 : B + (warp - HALF) * 4096);
+}
+
+// ---- ring + shared-memory plan --------------------------------------------
+
+struct Plan {
+  uint32_t tb;       // bytes per slot
+  int ns;            // slots
+  uint32_t off_ring, off_mat, off_inv, off_flag, off_misc, off_bar, bytes;
+  // mats: forward S (4 KB); backward S^T, dA, dA^T (12 KB)
+  __host__ __device__ Plan(int N, int NS, bool bwd) {
+    tb = tile_bytes(N);
+    ns = NS;
+    off_ring = 0;
+    off_mat = off_ring + (uint32_t)NS * tb;
+    off_inv = off_mat + (bwd ? 2 * 4096 : 4096);  // bwd: [S^T | dA^T] overlay, then dA
+    off_flag = off_inv + (bwd ? 2 * kMaxN * 4 : 0);
+    off_misc = off_flag + kMaxN;  // per-warp counts (8 ints), then dm partials (8 doubles)
+    off_bar = off_misc + 32 + 8 * 8;
+    bytes = off_bar + 2 * 8 * (uint32_t)NS;  // full[NS], empty[NS]
+  }
+};
+
+struct RingPos {
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next(int ns) {
+    if (++slot == ns) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+// Zero rows [N, round8(N)) of every slot once, so row-reductions may run
+// whole 8-row groups and row-outputs never read uninitialised memory.
+__host__ __device__ constexpr uint32_t tail_end(int N) { return (uint32_t)(N + 7) / 8u * 8u * kRowBytes; }
+
+__device__ __forceinline__ void zero_tails(uint8_t* ring, const Plan& pl, int N, int tid,
+                                           int nthreads) {
+  const uint32_t lo = (uint32_t)N * kRowBytes;
+  const uint32_t per = (tail_end(N) - lo) / 16;
+  for (uint32_t i = tid; i < per * (uint32_t)pl.ns; i += nthreads) {
+    const uint32_t s = i / per, k = i - s * per;
+    st4(ring + s * pl.tb + lo + 16 * k, make_float4(0.f, 0.f, 0.f, 0.f));
+  }
+}
+
+// Consumer-side, one unit ahead: the valid flag of row tid of unit u's
+// sequence (registers; consumed by publish_flags at the next unit).
+__device__ __forceinline__ int fetch_flag(const OpParams& p, int u, int units, int tid) {
+  if (u >= units || tid >= (int)p.N) return 0;
+  if (p.valid == nullptr) return 1;
+  const int64_t b = u / (int)p.H;
+  return __ldg(p.valid + b * p.msb + tid) != 0;
+}
+// Saved S of unit u (backward), one unit ahead: element pairs (a, c4..c4+3).
+template <int PERS, int NW>
+__device__ __forceinline__ void fetch_S(const OpParams& p, int u, int units, int tid,
+                                        float4 (&sr)[PERS]) {
+  if (u >= units) return;
+  const float* gS = static_cast<const float*>(p.saved_S) + (int64_t)u * 1024;
+#pragma unroll
+  for (int k = 0; k < PERS; ++k) {
+    const int i = tid + k * NW * 32;
+    if (i < 256) sr[k] = __ldg(reinterpret_cast<const float4*>(gS + (i & 31) * 32 + (i >> 5) * 4));
+  }
+}
+// Valid flags into flag[] and true_n (attention.cpp:26-33); one consumer sync.
+template <int NW>
+__device__ __forceinline__ int publish_flags(int f, int N, uint8_t* flag, int* cnt, int tid) {
+  if (tid < N) flag[tid] = (uint8_t)f;  // NW*32 >= N
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  if ((tid & 31) == 0) cnt[tid >> 5] = __popc(m);
+  consumer_sync<NW>();
   int n = 0;
 #pragma unroll
-  for (int k = 0; k < kMaxN / 32; ++k) {
-    if (k >= nc) break;
-    const uint32_t w = __ballot_sync(0xffffffffu, (fr[k >> 2] >> (8 * (k & 3))) & 1u);
-    if (lane == 0) flagw[k] = w;
-    n += __popc(w);
-  }
-  __syncwarp();
+  for (int w = 0; w < NW; ++w) n += cnt[w];
   return n;
 }
 
 // ---- forward ---------------------------------------------------------------
 
-template <int NSTG>
-__global__ void __launch_bounds__(256) cos_fwd_d32_kernel(
+template <int NW, int NS>
+__global__ void __launch_bounds__((NW + 1) * 32) cos_fwd_d32_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, const OpParams p,
     const __grid_constant__ ScaleTable tab) {
-  using PL = WarpPlan<false, NSTG>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wpc = blockDim.x >> 5;
-  uint8_t* ws = smem + warp * PL::bytes;
-  float* Sm = reinterpret_cast<float*>(ws + PL::off_mat);
-  uint32_t* flagw = reinterpret_cast<uint32_t*>(ws + PL::off_flag);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ws + PL::off_bar);
-
   const int N = (int)p.N, H = (int)p.H;
   const int units = (int)(p.B * p.H);
-  const int nc = (N + 31) / 32;
-  const int gw = blockIdx.x * wpc + warp, tw = gridDim.x * wpc;
+  const Plan pl(N, NS, false);
+  uint8_t* ring = smem + pl.off_ring;
+  float* Ss = reinterpret_cast<float*>(smem + pl.off_mat);
+  uint8_t* flag = smem + pl.off_flag;
+  int* cnt = reinterpret_cast<int*>(smem + pl.off_misc);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
+  uint64_t* empty = full + NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bytes = (uint32_t)N * kRowBytes;
   float* O = static_cast<float*>(p.out);
   float* norms_all = static_cast<float*>(p.saved_norms);
-  float* gS_all = static_cast<float*>(p.saved_S);
   const bool want_q = O != nullptr || norms_all != nullptr;
-  const int J = want_q ? 2 * nc : nc;  // jobs (chunk loads) per unit
-  const int my_units = gw < units ? (units - 1 - gw) / tw + 1 : 0;
-  const long total = (long)my_units * J;
-  if (my_units == 0) return;
 
-  if (lane == 0) {
-    for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
-    fence_barrier_init();
-    prefetch_map(&tk);
-    prefetch_map(&tv);
-    if (want_q) prefetch_map(&tq);
-  }
-  __syncwarp();
-  // Lane 0: load job j (chunk t of this warp's k-th unit) into stage j % NSTG.
-  auto issue = [&](long j) {
-    if (j >= total) return;
-    const int k = (int)(j / J), t = (int)(j - (long)k * J);
-    const int u = gw + k * tw;
-    const int b = u / H, h = u - b * H;
-    const int s = (int)(j % NSTG);
-    uint8_t* st = ws + s * PL::kStage;
-    if (t < nc) {
-      mbar_expect_tx(&bar[s], 2 * kTile);
-      tma_load_4d(st, &tk, 0, 32 * t, h, b, &bar[s]);
-      tma_load_4d(st + kTile, &tv, 0, 32 * t, h, b, &bar[s]);
-    } else {
-      mbar_expect_tx(&bar[s], kTile);
-      tma_load_4d(st, &tq, 0, 32 * (t - nc), h, b, &bar[s]);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
     }
-  };
-  if (lane == 0)
-    for (int j = 0; j < NSTG; ++j) issue(j);
+    fence_barrier_init();
+  }
+  zero_tails(ring, pl, N, threadIdx.x, blockDim.x);
+  __syncthreads();
 
+  if (warp == NW) {  // ===== producer =====
+    if (lane == 0) {
+      prefetch_map(&tk);
+      prefetch_map(&tv);
+      prefetch_map(&tq);
+      RingPos pos;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int t = 0; t < (want_q ? 3 : 2); ++t) {
+          mbar_wait(&empty[pos.slot], pos.phase ^ 1u);
+          mbar_expect_tx(&full[pos.slot], bytes);
+          tma_load_4d(ring + pos.slot * pl.tb, t == 0 ? &tk : t == 1 ? &tv : &tq, 0, 0, h, b,
+                      &full[pos.slot]);
+          pos.next(NS);
+        }
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int tid = threadIdx.x;
   const float eps = (float)p.eps;
+  const int r0 = warp * 32;
   const int rg = lane >> 2, cg = lane & 3;
-  uint32_t fnext[kMaxN / 128];
-  fetch_flags(p, gw, units, nc, lane, fnext);
-  long j = 0;
-  for (int k = 0; k < my_units; ++k) {
-    const int u = gw + k * tw;
+  float* gS_all = static_cast<float*>(p.saved_S);
+  RingPos pos;
+  int fnext = fetch_flag(p, blockIdx.x, units, tid);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int b = u / H, h = u - b * H;
-    uint32_t fcur[kMaxN / 128];
-#pragma unroll
-    for (int i = 0; i < kMaxN / 128; ++i) fcur[i] = fnext[i];
-    fetch_flags(p, u + tw, units, nc, lane, fnext);  // next unit, hidden behind this one
-    const int true_n = publish_flags(fcur, nc, flagw, lane);
-    if (true_n == 0 && lane == 0 && p.status) atomicOr(p.status, 1);  // :44 (NaN outputs)
+    const int fcur = fnext;
+    fnext = fetch_flag(p, u + gridDim.x, units, tid);  // hidden behind this unit
+    const int sk = pos.slot;
+    const uint32_t phk = pos.phase;
+    pos.next(NS);
+    const int sv = pos.slot;
+    const uint32_t phv = pos.phase;
+    pos.next(NS);
+    int sq = -1;
+    uint32_t phq = 0;
+    if (want_q) {
+      sq = pos.slot;
+      phq = pos.phase;
+      pos.next(NS);
+    }
+    uint8_t* Kt = ring + sk * pl.tb;
+    uint8_t* Vt = ring + sv * pl.tb;
+    const int true_n = publish_flags<NW>(fcur, N, flag, cnt, tid);
     const int64_t base = (int64_t)b * p.sb + (int64_t)h * p.sh;
     float* norms = norms_all ? norms_all + (int64_t)u * 2 * N : nullptr;
+    if (true_n == 0) {  // UsageError in the reference (attention.cpp:44): NaN outputs
+      if (tid == 0 && p.status) atomicOr(p.status, 1);
+      if (O)
+        for (int i = tid; i < N * kD; i += NW * 32)
+          O[base + (int64_t)(i / kD) * p.sn + (i % kD)] = __int_as_float(0x7fc00000);
+      mbar_wait(&full[sk], phk);
+      mbar_wait(&full[sv], phv);
+      if (sq >= 0) mbar_wait(&full[sq], phq);
+      consumer_sync<NW>();
+      if (tid == 0) {
+        mbar_arrive(&empty[sk]);
+        mbar_arrive(&empty[sv]);
+        if (sq >= 0) mbar_arrive(&empty[sq]);
+      }
+      continue;
+    }
 
-    // Pass 1 (:328-361): S = K~^T V, streamed over 32-row chunks.
+    // Pass 1 (:328-361): S = K~^T V.
     float2 acc[4][4];
 #pragma unroll
     for (int y = 0; y < 4; ++y)
 #pragma unroll
       for (int x = 0; x < 4; ++x) acc[y][x] = f2(0.f, 0.f);
-    for (int c = 0; c < nc; ++c, ++j) {
-      const int s = (int)(j % NSTG);
-      mbar_wait(&bar[s], (uint32_t)((j / NSTG) & 1));
-      uint8_t* Kt = ws + s * PL::kStage;
-      const int rows = min(32, N - 32 * c);
-      normalize_tile(Kt, rows, flagw[c], eps, nullptr, norms ? norms + N + 32 * c : nullptr,
-                     lane);
-      __syncwarp();
-      row_reduce_tile(Kt, Kt + kTile, rows, acc, lane);
-      __syncwarp();
-      if (lane == 0) {
-        fence_proxy_async();
-        issue(j + NSTG);
+    mbar_wait(&full[sk], phk);
+    mbar_wait(&full[sv], phv);
+    normalize_rows(Kt, r0, N, flag, eps, nullptr, norms ? norms + N : nullptr, lane);
+    __syncwarp();
+    row_reduce(Kt, Vt, r0, N, acc, lane);
+    consumer_sync<NW>();  // every warp done with K~, V: partials overlay them
+    store_partial(partial_slot<NW>(Kt, Vt, warp), acc, lane);
+    consumer_sync<NW>();
+    {
+      constexpr int PER = (256 + NW * 32 - 1) / (NW * 32);
+      float4 s4[PER];
+      reduce_partials<NW, PER>(reinterpret_cast<float*>(Kt), reinterpret_cast<float*>(Vt), tid,
+                               s4);
+      float* gS = gS_all ? gS_all + (int64_t)u * 1024 : nullptr;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e4 = tid + k * NW * 32;
+        if (e4 < 256) {
+          reinterpret_cast<float4*>(Ss)[e4] = s4[k];
+          if (gS) reinterpret_cast<float4*>(gS)[e4] = s4[k];
+        }
       }
     }
-    store_rowmajor(Sm, acc, 1.0f, lane);
-    __syncwarp();
-    if (gS_all) {  // saved state for the backward
-      float4* dst = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dst[lane + 32 * i] = reinterpret_cast<const float4*>(Sm)[lane + 32 * i];
+    if (N * kRowBytes < (uint32_t)((NW + 1) / 2) * 4096u) {  // partials spilled into tails
+      consumer_sync<NW>();
+      for (int i = tid; i < (int)((tail_end(N) - N * kRowBytes) / 16); i += NW * 32) {
+        st4(Kt + N * kRowBytes + 16 * i, make_float4(0.f, 0.f, 0.f, 0.f));
+        st4(Vt + N * kRowBytes + 16 * i, make_float4(0.f, 0.f, 0.f, 0.f));
+      }
+    }
+    consumer_sync<NW>();  // S complete; K, V slots free
+    if (tid == 0) {
+      mbar_arrive(&empty[sk]);
+      mbar_arrive(&empty[sv]);
     }
     if (!want_q) continue;
 
     // Pass 2 (:363-388): O = s * Q~ S for every row (padded rows included).
-    const float scale = true_n > 0 ? scale_of(tab, true_n, p.m) : __int_as_float(0x7fc00000);
-    for (int c = 0; c < nc; ++c, ++j) {
-      const int s = (int)(j % NSTG);
-      mbar_wait(&bar[s], (uint32_t)((j / NSTG) & 1));
-      const uint8_t* Qt = ws + s * PL::kStage;
-      float2 o[4][4];
-      row_output_tile(Qt, Sm, o, lane);
+    uint8_t* Qt = ring + sq * pl.tb;
+    const float scale = tab.s[true_n];
+    mbar_wait(&full[sq], phq);
+    float2 o[4][4];
+    row_output(Qt, Ss, r0, o, lane);
+    float* orow = O ? O + base + (int64_t)(r0 + rg) * p.sn : nullptr;
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int r = 32 * c + rg + 8 * jj;
-        float qv[8];
-        own_cols(Qt, jj, lane, qv);
-        float ss = 0.f;
+    for (int j = 0; j < 4; ++j) {
+      const int r = r0 + rg + 8 * j;
+      float qv[8];
+      own_cols(Qt, r0, j, lane, qv);
+      float ss = 0.f;
 #pragma unroll
-        for (int x = 0; x < 8; ++x) ss = fmaf(qv[x], qv[x], ss);
-        ss = row_sum4(ss);
-        const float nrm = sqrtf(ss + eps);
-        const float w = scale * (1.0f / nrm);
-        if (r < N) {
-          float v[8];
-          unpack(o[jj], v);
+      for (int x = 0; x < 8; ++x) ss = fmaf(qv[x], qv[x], ss);
+      ss = row_sum4(ss);
+      const float nrm = sqrtf(ss + eps);
+      const float w = scale * (1.0f / nrm);
+      if (r < N) {
+        float v[8];
+        unpack(o[j], v);
 #pragma unroll
-          for (int x = 0; x < 8; ++x) v[x] *= w;
-          if (O) store_row(O + base + (int64_t)r * p.sn, cg, v);
-          if (norms && cg == 0) norms[r] = nrm;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        fence_proxy_async();
-        issue(j + NSTG);
+        for (int x = 0; x < 8; ++x) v[x] *= w;
+        if (orow) store_row(orow + (int64_t)8 * j * p.sn, cg, v);
+        if (norms && cg == 0) norms[r] = nrm;
       }
     }
+    consumer_sync<NW>();  // Q slot, S and flags free for the next unit
+    if (tid == 0) mbar_arrive(&empty[sq]);
   }
 }
 
 // ---- backward ----------------------------------------------------------------
 
-template <int NSTG>
-__global__ void __launch_bounds__(256) cos_bwd_d32_kernel(
+template <int NW, int NS>
+__global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
     const OpParams p, const __grid_constant__ ScaleTable tab) {
-  using PL = WarpPlan<true, NSTG>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wpc = blockDim.x >> 5;
-  uint8_t* ws = smem + warp * PL::bytes;
-  float* St = reinterpret_cast<float*>(ws + PL::off_mat);  // S^T, later dA^T
-  float* dAt = St;
-  float* dA = reinterpret_cast<float*>(ws + PL::off_mat2);
-  float* inv = reinterpret_cast<float*>(ws + PL::off_inv);
-  uint32_t* flagw = reinterpret_cast<uint32_t*>(ws + PL::off_flag);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ws + PL::off_bar);
-
   const int N = (int)p.N, H = (int)p.H;
   const int units = (int)(p.B * p.H);
-  const int nc = (N + 31) / 32;
-  const int gw = blockIdx.x * wpc + warp, tw = gridDim.x * wpc;
-  const int J = 2 * nc;
-  const int my_units = gw < units ? (units - 1 - gw) / tw + 1 : 0;
-  const long total = (long)my_units * J;
-  if (my_units == 0) return;
+  const Plan pl(N, NS, true);
+  uint8_t* ring = smem + pl.off_ring;
+  float* St = reinterpret_cast<float*>(smem + pl.off_mat);
+  float* dA = St + 1024;
+  float* dAt = St;  // S^T is dead once <G,S> is taken; dA^T reuses it
+  float* inv_q = reinterpret_cast<float*>(smem + pl.off_inv);
+  float* inv_k = inv_q + kMaxN;
+  uint8_t* flag = smem + pl.off_flag;
+  int* cnt = reinterpret_cast<int*>(smem + pl.off_misc);
+  double* red = reinterpret_cast<double*>(smem + pl.off_misc + 32);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
+  uint64_t* empty = full + NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bytes = (uint32_t)N * kRowBytes;
 
-  if (lane == 0) {
-    for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
     fence_barrier_init();
-    prefetch_map(&tq);
-    prefetch_map(&tdo);
-    prefetch_map(&tk);
-    prefetch_map(&tv);
   }
-  __syncwarp();
-  auto issue = [&](long j) {  // lane 0: phase A chunks (Q, dO), then phase B (K, V)
-    if (j >= total) return;
-    const int k = (int)(j / J), t = (int)(j - (long)k * J);
-    const int u = gw + k * tw;
-    const int b = u / H, h = u - b * H;
-    const int s = (int)(j % NSTG);
-    uint8_t* st = ws + s * PL::kStage;
-    const bool a = t < nc;
-    const int row = 32 * (a ? t : t - nc);
-    mbar_expect_tx(&bar[s], 2 * kTile);
-    tma_load_4d(st, a ? &tq : &tk, 0, row, h, b, &bar[s]);
-    tma_load_4d(st + kTile, a ? &tdo : &tv, 0, row, h, b, &bar[s]);
-  };
-  if (lane == 0)
-    for (int j = 0; j < NSTG; ++j) issue(j);
+  zero_tails(ring, pl, N, threadIdx.x, blockDim.x);
+  __syncthreads();
 
+  if (warp == NW) {  // ===== producer: Q, dO, K, V per unit =====
+    if (lane == 0) {
+      prefetch_map(&tq);
+      prefetch_map(&tdo);
+      prefetch_map(&tk);
+      prefetch_map(&tv);
+      RingPos pos;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int t = 0; t < 4; ++t) {
+          mbar_wait(&empty[pos.slot], pos.phase ^ 1u);
+          mbar_expect_tx(&full[pos.slot], bytes);
+          const CUtensorMap* m = t == 0 ? &tq : t == 1 ? &tdo : t == 2 ? &tk : &tv;
+          tma_load_4d(ring + pos.slot * pl.tb, m, 0, 0, h, b, &full[pos.slot]);
+          pos.next(NS);
+        }
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int tid = threadIdx.x;
   const float eps = (float)p.eps;
+  const int r0 = warp * 32;
   const int rg = lane >> 2, cg = lane & 3;
-  const int ag = lane >> 3, bg = lane & 7;
   float* dQ = static_cast<float*>(p.dq);
   float* dK = static_cast<float*>(p.dk);
   float* dV = static_cast<float*>(p.dv);
-  const float* gS_all = static_cast<const float*>(p.saved_S);
-  uint32_t fnext[kMaxN / 128];
-  fetch_flags(p, gw, units, nc, lane, fnext);
-  float4 snext[8];  // row `lane` of the next unit's saved S
-  {
-    const float4* src = reinterpret_cast<const float4*>(gS_all + (int64_t)gw * 1024 + lane * 32);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) snext[i] = __ldg(src + i);
-  }
-  long j = 0;
-  for (int k = 0; k < my_units; ++k) {
-    const int u = gw + k * tw;
+  RingPos pos;
+  constexpr int PERS = (256 + NW * 32 - 1) / (NW * 32);
+  float4 snext[PERS];
+  fetch_S<PERS, NW>(p, blockIdx.x, units, tid, snext);
+  int fnext = fetch_flag(p, blockIdx.x, units, tid);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int b = u / H, h = u - b * H;
-    // S^T[c][a] = S[a][c]: lane a writes column a (conflict-free).
+    // S^T from the prefetched saved state: St[c][a] = S[a][c] (a = lane: conflict-free)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      St[(4 * i + 0) * 32 + lane] = snext[i].x;
-      St[(4 * i + 1) * 32 + lane] = snext[i].y;
-      St[(4 * i + 2) * 32 + lane] = snext[i].z;
-      St[(4 * i + 3) * 32 + lane] = snext[i].w;
+    for (int k = 0; k < PERS; ++k) {
+      const int i = tid + k * NW * 32;
+      if (i < 256) {
+        const int a = i & 31, c4 = (i >> 5) * 4;
+        St[(c4 + 0) * 32 + a] = snext[k].x;
+        St[(c4 + 1) * 32 + a] = snext[k].y;
+        St[(c4 + 2) * 32 + a] = snext[k].z;
+        St[(c4 + 3) * 32 + a] = snext[k].w;
+      }
     }
-    uint32_t fcur[kMaxN / 128];
-#pragma unroll
-    for (int i = 0; i < kMaxN / 128; ++i) fcur[i] = fnext[i];
-    if (u + tw < units) {  // next unit's flags and S, hidden behind this unit
-      fetch_flags(p, u + tw, units, nc, lane, fnext);
-      const float4* src =
-          reinterpret_cast<const float4*>(gS_all + (int64_t)(u + tw) * 1024 + lane * 32);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) snext[i] = __ldg(src + i);
+    const int fcur = fnext;
+    fetch_S<PERS, NW>(p, u + gridDim.x, units, tid, snext);  // next unit, hidden behind this one
+    fnext = fetch_flag(p, u + gridDim.x, units, tid);
+    int sl[4];
+    uint32_t ph[4];
+    for (int t = 0; t < 4; ++t) {
+      sl[t] = pos.slot;
+      ph[t] = pos.phase;
+      pos.next(NS);
     }
-    const int true_n = publish_flags(fcur, nc, flagw, lane);  // includes __syncwarp
-    if (true_n == 0 && lane == 0) {
-      if (p.status) atomicOr(p.status, 1);
-    }
-    const float scale = true_n > 0 ? scale_of(tab, true_n, p.m) : __int_as_float(0x7fc00000);
+    uint8_t* Qt = ring + sl[0] * pl.tb;
+    uint8_t* Gt = ring + sl[1] * pl.tb;  // dO
+    uint8_t* Kt = ring + sl[2] * pl.tb;
+    uint8_t* Vt = ring + sl[3] * pl.tb;
+    const int true_n = publish_flags<NW>(fcur, N, flag, cnt, tid);  // includes a consumer sync
     const int64_t base = (int64_t)b * p.sb + (int64_t)h * p.sh;
+    if (true_n == 0) {
+      if (tid == 0) {
+        if (p.status) atomicOr(p.status, 1);
+        if (p.dm_unit) p.dm_unit[u] = __longlong_as_double(0x7ff8000000000000ll);
+      }
+      const float qnan = __int_as_float(0x7fc00000);
+      for (int i = tid; i < N * kD; i += NW * 32) {
+        const int64_t o = base + (int64_t)(i / kD) * p.sn + (i % kD);
+        dQ[o] = qnan;
+        dK[o] = qnan;
+        dV[o] = qnan;
+      }
+      for (int t = 0; t < 4; ++t) mbar_wait(&full[sl[t]], ph[t]);
+      consumer_sync<NW>();
+      if (tid == 0)
+        for (int t = 0; t < 4; ++t) mbar_arrive(&empty[sl[t]]);
+      continue;
+    }
+    const float scale = tab.s[true_n];
 
-    // Phase A: dQ (:410-411, :421-428) and G = Q~^T dO (:405), every row.
-    float2 acc[4][4];
-#pragma unroll
-    for (int y = 0; y < 4; ++y)
-#pragma unroll
-      for (int x = 0; x < 4; ++x) acc[y][x] = f2(0.f, 0.f);
-    for (int c = 0; c < nc; ++c, ++j) {
-      const int s = (int)(j % NSTG);
-      mbar_wait(&bar[s], (uint32_t)((j / NSTG) & 1));
-      uint8_t* Qt = ws + s * PL::kStage;
-      const uint8_t* Gt = Qt + kTile;  // dO
-      const int rows = min(32, N - 32 * c);
-      normalize_tile(Qt, rows, 0xffffffffu, eps, inv, nullptr, lane);
-      __syncwarp();
+    // Phase A: dQ (:410-411, :421-428) then G = Q~^T dO (:405), every row.
+    mbar_wait(&full[sl[0]], ph[0]);
+    mbar_wait(&full[sl[1]], ph[1]);
+    normalize_rows(Qt, r0, N, nullptr, eps, inv_q, nullptr, lane);
+    __syncwarp();
+    {
       float2 o[4][4];
-      row_output_tile(Gt, St, o, lane);  // dO S^T (unscaled)
+      row_output(Gt, St, r0, o, lane);  // dO S^T (unscaled)
+      float* drow = dQ + base + (int64_t)(r0 + rg) * p.sn;
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int rl = rg + 8 * jj;
-        const int r = 32 * c + rl;
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + rg + 8 * j;
         float g[8], qh[8];
-        unpack(o[jj], g);
-        own_cols(Qt, jj, lane, qh);
+        unpack(o[j], g);
+        own_cols(Qt, r0, j, lane, qh);
         float pr = 0.f;
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
@@ -582,108 +684,130 @@ __global__ void __launch_bounds__(256) cos_bwd_d32_kernel(
         }
         pr = row_sum4(pr);
         if (r < N) {
-          const float iv = inv[rl];
+          const float iv = inv_q[r];
 #pragma unroll
           for (int x = 0; x < 8; ++x) g[x] = (g[x] - pr * qh[x]) * iv;
-          store_row(dQ + base + (int64_t)r * p.sn, cg, g);
+          store_row(drow + (int64_t)8 * j * p.sn, cg, g);
         }
       }
-      row_reduce_tile(Qt, Gt, rows, acc, lane);
-      __syncwarp();
-      if (lane == 0) {
-        fence_proxy_async();
-        issue(j + NSTG);
-      }
     }
-    // dm = -ln(n) s <G, S> (:408): lane's block of G against S[a][b] = S^T[b][a].
-    {
-      float d = 0.f;
+    float2 acc[4][4];
 #pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        const float* row = St + (4 * bg + y) * 32 + 8 * ag;
-        const float4 s0 = *reinterpret_cast<const float4*>(row);
-        const float4 s1 = *reinterpret_cast<const float4*>(row + 4);
-        d = fmaf(acc[y][0].x, s0.x, d);
-        d = fmaf(acc[y][0].y, s0.y, d);
-        d = fmaf(acc[y][1].x, s0.z, d);
-        d = fmaf(acc[y][1].y, s0.w, d);
-        d = fmaf(acc[y][2].x, s1.x, d);
-        d = fmaf(acc[y][2].y, s1.y, d);
-        d = fmaf(acc[y][3].x, s1.z, d);
-        d = fmaf(acc[y][3].y, s1.w, d);
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) acc[y][x] = f2(0.f, 0.f);
+    row_reduce(Qt, Gt, r0, N, acc, lane);
+    consumer_sync<NW>();  // Q~, dO dead: partials overlay them
+    store_partial(partial_slot<NW>(Qt, Gt, warp), acc, lane);
+    consumer_sync<NW>();
+    {
+      constexpr int PER = (256 + NW * 32 - 1) / (NW * 32);
+      float4 g4[PER];
+      reduce_partials<NW, PER>(reinterpret_cast<float*>(Qt), reinterpret_cast<float*>(Gt), tid,
+                               g4);
+      double dot = 0.0;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e4 = tid + k * NW * 32;
+        if (e4 < 256) {
+          const int a = e4 >> 3, c = (e4 & 7) * 4;  // <G, S> (:408)
+          float d = g4[k].x * St[(c + 0) * 32 + a];
+          d = fmaf(g4[k].y, St[(c + 1) * 32 + a], d);
+          d = fmaf(g4[k].z, St[(c + 2) * 32 + a], d);
+          d = fmaf(g4[k].w, St[(c + 3) * 32 + a], d);
+          dot += (double)d;
+        }
       }
-      double dot = (double)d;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (lane == 0 && p.dm_unit)
-        p.dm_unit[u] = true_n > 0 ? coef_of(tab, true_n, p.m) * dot
-                                  : __longlong_as_double(0x7ff8000000000000ll);
+      consumer_sync<NW>();  // partials and S^T read: both regions may now be overwritten
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e4 = tid + k * NW * 32;
+        if (e4 < 256) {
+          const int a = e4 >> 3, c = (e4 & 7) * 4;
+          const float4 s = make_float4(g4[k].x * scale, g4[k].y * scale, g4[k].z * scale,
+                                       g4[k].w * scale);  // dA = s G (:412-413)
+          reinterpret_cast<float4*>(dA)[e4] = s;
+          dAt[(c + 0) * 32 + a] = s.x;
+          dAt[(c + 1) * 32 + a] = s.y;
+          dAt[(c + 2) * 32 + a] = s.z;
+          dAt[(c + 3) * 32 + a] = s.w;
+        }
+      }
+      if (N * kRowBytes < (uint32_t)((NW + 1) / 2) * 4096u)  // partials spilled into tails
+        for (int i = tid; i < (int)((tail_end(N) - N * kRowBytes) / 16); i += NW * 32) {
+          st4(Qt + N * kRowBytes + 16 * i, make_float4(0.f, 0.f, 0.f, 0.f));
+          st4(Gt + N * kRowBytes + 16 * i, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+      consumer_sync<NW>();  // dA complete; Q, dO slots free
+      if (lane == 0) red[warp] = dot;
+      if (tid == 0) {
+        mbar_arrive(&empty[sl[0]]);
+        mbar_arrive(&empty[sl[1]]);
+      }
     }
-    __syncwarp();  // S^T reads done: dA^T may overwrite it
-    store_rowmajor(dA, acc, scale, lane);    // dA = s G (:412-413)
-    store_transposed(dAt, acc, scale, lane);
-    __syncwarp();
 
-    // Phase B: dV = K~ dA (:416), dK~ = V dA^T (:415) -> dK (:430-437); padded rows 0 (:439).
-    for (int c = 0; c < nc; ++c, ++j) {
-      const int s = (int)(j % NSTG);
-      mbar_wait(&bar[s], (uint32_t)((j / NSTG) & 1));
-      uint8_t* Kt = ws + s * PL::kStage;
-      const uint8_t* Vt = Kt + kTile;
-      const int rows = min(32, N - 32 * c);
-      const uint32_t vw = flagw[c];
-      float* krow = dK + base + (int64_t)(32 * c + rg) * p.sn;
-      float* vrow = dV + base + (int64_t)(32 * c + rg) * p.sn;
-      if (vw == 0u) {  // whole chunk padded: exact zeros, nothing to compute
+    // Phase B: dV = K~ dA (:416), dK~ = V dA^T (:415) -> dK (:430-437), padded rows 0 (:439).
+    mbar_wait(&full[sl[2]], ph[2]);
+    mbar_wait(&full[sl[3]], ph[3]);
+    {
+      const bool any_valid = __any_sync(0xffffffffu, r0 + lane < N && flag[r0 + lane] != 0);
+      float* krow = dK + base + (int64_t)(r0 + rg) * p.sn;
+      float* vrow = dV + base + (int64_t)(r0 + rg) * p.sn;
+      if (!any_valid) {  // whole block padded: exact zeros, nothing to compute
         const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-          if (rg + 8 * jj < rows) {
-            store_row(krow + (int64_t)8 * jj * p.sn, cg, z);
-            store_row(vrow + (int64_t)8 * jj * p.sn, cg, z);
+        for (int j = 0; j < 4; ++j)
+          if (r0 + rg + 8 * j < N) {
+            store_row(krow + (int64_t)8 * j * p.sn, cg, z);
+            store_row(vrow + (int64_t)8 * j * p.sn, cg, z);
           }
       } else {
-        normalize_tile(Kt, rows, vw, eps, inv, nullptr, lane);
+        normalize_rows(Kt, r0, N, flag, eps, inv_k, nullptr, lane);
         __syncwarp();
         float2 o[4][4];
-        row_output_tile(Kt, dA, o, lane);
+        row_output(Kt, dA, r0, o, lane);
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int rl = rg + 8 * jj;
-          if (rl < rows) {
+        for (int j = 0; j < 4; ++j) {
+          const int r = r0 + rg + 8 * j;
+          if (r < N) {
             float v[8];
-            unpack(o[jj], v);
-            if (!((vw >> rl) & 1u))
+            unpack(o[j], v);
+            if (!flag[r])
 #pragma unroll
               for (int x = 0; x < 8; ++x) v[x] = 0.f;
-            store_row(vrow + (int64_t)8 * jj * p.sn, cg, v);
+            store_row(vrow + (int64_t)8 * j * p.sn, cg, v);
           }
         }
-        row_output_tile(Vt, dAt, o, lane);
+        row_output(Vt, dAt, r0, o, lane);
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int rl = rg + 8 * jj;
+        for (int j = 0; j < 4; ++j) {
+          const int r = r0 + rg + 8 * j;
           float g[8], kh[8];
-          unpack(o[jj], g);
-          own_cols(Kt, jj, lane, kh);
+          unpack(o[j], g);
+          own_cols(Kt, r0, j, lane, kh);
           float pr = 0.f;
 #pragma unroll
           for (int x = 0; x < 8; ++x) pr = fmaf(g[x], kh[x], pr);
           pr = row_sum4(pr);
-          if (rl < rows) {
-            const bool valid = (vw >> rl) & 1u;
-            const float iv = inv[rl];
+          if (r < N) {
+            const bool valid = flag[r] != 0;
+            const float iv = inv_k[r];
 #pragma unroll
             for (int x = 0; x < 8; ++x) g[x] = valid ? (g[x] - pr * kh[x]) * iv : 0.f;
-            store_row(krow + (int64_t)8 * jj * p.sn, cg, g);
+            store_row(krow + (int64_t)8 * j * p.sn, cg, g);
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) {
-        fence_proxy_async();
-        issue(j + NSTG);
-      }
+    }
+    consumer_sync<NW>();  // K, V, dA, St, flags, red free for the next unit
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NW; ++w) t += red[w];
+      if (p.dm_unit) p.dm_unit[u] = tab.coef[true_n] * t;  // -ln(n) s <G,S> (:408)
+      mbar_arrive(&empty[sl[2]]);
+      mbar_arrive(&empty[sl[3]]);
     }
   }
 }
@@ -710,14 +834,13 @@ inline EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 4-D map over (D, N, H, B), (32, 32, 1, 1) box, 128-byte swizzle; rows past
-// N fall outside the map and are zero-filled.
+// 4-D map over (D, N, H, B) with a (32, N, 1, 1) box and 128-byte swizzle.
 inline bool make_unit_map(CUtensorMap* map, const void* base, const OpParams& p) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)p.N, (cuuint64_t)p.H, (cuuint64_t)p.B};
   cuuint64_t strides[3] = {(cuuint64_t)p.sn * 4, (cuuint64_t)p.sh * 4, (cuuint64_t)p.sb * 4};
-  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t box[4] = {32, (cuuint32_t)p.N, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -738,7 +861,7 @@ inline bool fast_fwd_supported(const OpParams& p) {
   if constexpr (!std::is_same<T, float>::value) {
     return false;
   } else {
-    return d32_layout_ok(p, {p.q, p.k, p.v, p.out, p.saved_S});
+    return d32_layout_ok(p, {p.q, p.k, p.v, p.out});
   }
 }
 template <typename T>
@@ -746,16 +869,13 @@ inline bool fast_bwd_supported(const OpParams& p) {
   if constexpr (!std::is_same<T, float>::value) {
     return false;
   } else {
-    return p.saved_S != nullptr &&
-           d32_layout_ok(p, {p.q, p.k, p.v, p.dout, p.dq, p.dk, p.dv, p.saved_S});
+    return p.saved_S != nullptr && d32_layout_ok(p, {p.q, p.k, p.v, p.dout, p.dq, p.dk, p.dv});
   }
 }
 
 inline d32::ScaleTable scale_table(double m, int N) {
   d32::ScaleTable t{};
-  t.s[0] = std::nanf("");
-  t.coef[0] = std::nan("");
-  for (int n = 1; n <= std::min(N, d32::kTabN); ++n) {
+  for (int n = 1; n <= N; ++n) {
     const double ln = std::log(static_cast<double>(n));
     const double s = std::exp(-m * ln);  // attention.cpp:304 / :403, in fp64
     t.s[n] = static_cast<float>(s);
@@ -774,33 +894,95 @@ inline int sm_count() {
   return n;
 }
 
-// Persistent launch: one CTA per SM with as many unit-warps as fit in shared
-// memory (<= 8), but never more warps than units.
+// Launch a persistent ring kernel: NS = ring slots.  Grid = resident CTAs.
 template <typename Kern, typename... Args>
-inline cudaError_t launch_warps(Kern kern, uint32_t per_warp, int units, cudaStream_t st,
-                                Args... args) {
-  const int wpc = std::max(1, std::min<int>(8, (int)((227u * 1024u) / per_warp)));
-  const int total = std::min(units, wpc * sm_count());
-  const int grid = (total + wpc - 1) / wpc;
-  const uint32_t smem = per_warp * (uint32_t)wpc;
+inline cudaError_t launch_persistent(Kern kern, int threads, uint32_t smem, int units,
+                                     cudaStream_t st, Args... args) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, wpc * 32, smem, st>>>(args...);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int grid = std::min(units, per_sm * sm_count());
+  kern<<<grid, threads, smem, st>>>(args...);
   return cudaGetLastError();
 }
 
-constexpr int kFwdStages = 3;
-constexpr int kBwdStages = 3;
+// Ring depth: as many tile slots as fit in `budget` bytes, at least `min_ns`.
+inline int pick_slots(int N, bool bwd, uint32_t budget, int min_ns, int max_ns) {
+  int ns = max_ns;
+  while (ns > min_ns && d32::Plan(N, ns, bwd).bytes > budget) --ns;
+  return ns;
+}
 
+template <int NW, int NS>
+inline cudaError_t fwd_nw_ns(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                             const OpParams& p, const d32::ScaleTable& tab, cudaStream_t st) {
+  const d32::Plan pl((int)p.N, NS, false);
+  return launch_persistent(d32::cos_fwd_d32_kernel<NW, NS>, (NW + 1) * 32, pl.bytes,
+                           (int)(p.B * p.H), st, q, k, v, p, tab);
+}
+template <int NW, int NS>
+inline cudaError_t bwd_nw_ns(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                             const CUtensorMap& g, const OpParams& p, const d32::ScaleTable& tab,
+                             cudaStream_t st) {
+  const d32::Plan pl((int)p.N, NS, true);
+  return launch_persistent(d32::cos_bwd_d32_kernel<NW, NS>, (NW + 1) * 32, pl.bytes,
+                           (int)(p.B * p.H), st, q, k, v, g, p, tab);
+}
+
+// Slot counts per kernel are chosen so that two CTAs fit per SM for the long
+// tiles (N > 128: fwd 4 slots, bwd 8 slots with one CTA) and several for short.
+template <int NW>
+inline cudaError_t fwd_nw(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                          const OpParams& p, const d32::ScaleTable& tab, cudaStream_t st) {
+  const int N = (int)p.N;
+  const int ns = pick_slots(N, false, 113 * 1024, 3, 6);
+  switch (ns) {
+    case 3: return fwd_nw_ns<NW, 3>(q, k, v, p, tab, st);
+    case 4: return fwd_nw_ns<NW, 4>(q, k, v, p, tab, st);
+    case 5: return fwd_nw_ns<NW, 5>(q, k, v, p, tab, st);
+    default: return fwd_nw_ns<NW, 6>(q, k, v, p, tab, st);
+  }
+}
+template <int NW>
+inline cudaError_t bwd_nw(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                          const CUtensorMap& g, const OpParams& p, const d32::ScaleTable& tab,
+                          cudaStream_t st) {
+  const int N = (int)p.N;
+  // two (or more) CTAs per SM when a whole unit's 4 tiles fit in half the SM,
+  // else one CTA with up to 8 slots
+  const uint32_t budget = d32::Plan(N, 4, true).bytes <= 113 * 1024 ? 113 * 1024 : 227 * 1024;
+  const int ns = pick_slots(N, true, budget, 4, 8);
+  switch (ns) {
+    case 4: return bwd_nw_ns<NW, 4>(q, k, v, g, p, tab, st);
+    case 5: return bwd_nw_ns<NW, 5>(q, k, v, g, p, tab, st);
+    case 6: return bwd_nw_ns<NW, 6>(q, k, v, g, p, tab, st);
+    case 7: return bwd_nw_ns<NW, 7>(q, k, v, g, p, tab, st);
+    default: return bwd_nw_ns<NW, 8>(q, k, v, g, p, tab, st);
+  }
+}
+
+// Returns the number of kernel launches (1), or -1 if a tensor map could not
+// be encoded (the caller reports cudaGetLastError() first).
 template <typename T>
 inline int launch_fast_fwd(const OpParams& p, cudaStream_t st) {
   CUtensorMap mq, mk, mv;
   if (!make_unit_map(&mq, p.q, p) || !make_unit_map(&mk, p.k, p) || !make_unit_map(&mv, p.v, p))
     return -1;
   const d32::ScaleTable tab = scale_table(p.m, (int)p.N);
-  const cudaError_t e = launch_warps(d32::cos_fwd_d32_kernel<kFwdStages>,
-                                     d32::WarpPlan<false, kFwdStages>::bytes, (int)(p.B * p.H), st,
-                                     mq, mk, mv, p, tab);
+  cudaError_t e;
+  switch ((int)((p.N + 31) / 32)) {
+    case 1: e = fwd_nw<1>(mq, mk, mv, p, tab, st); break;
+    case 2: e = fwd_nw<2>(mq, mk, mv, p, tab, st); break;
+    case 3: e = fwd_nw<3>(mq, mk, mv, p, tab, st); break;
+    case 4: e = fwd_nw<4>(mq, mk, mv, p, tab, st); break;
+    case 5: e = fwd_nw<5>(mq, mk, mv, p, tab, st); break;
+    case 6: e = fwd_nw<6>(mq, mk, mv, p, tab, st); break;
+    case 7: e = fwd_nw<7>(mq, mk, mv, p, tab, st); break;
+    default: e = fwd_nw<8>(mq, mk, mv, p, tab, st); break;
+  }
   return e == cudaSuccess ? 1 : -1;
 }
 template <typename T>
@@ -810,9 +992,17 @@ inline int launch_fast_bwd(const OpParams& p, cudaStream_t st) {
       !make_unit_map(&mv, p.v, p) || !make_unit_map(&mg, p.dout, p))
     return -1;
   const d32::ScaleTable tab = scale_table(p.m, (int)p.N);
-  const cudaError_t e = launch_warps(d32::cos_bwd_d32_kernel<kBwdStages>,
-                                     d32::WarpPlan<true, kBwdStages>::bytes, (int)(p.B * p.H), st,
-                                     mq, mk, mv, mg, p, tab);
+  cudaError_t e;
+  switch ((int)((p.N + 31) / 32)) {
+    case 1: e = bwd_nw<1>(mq, mk, mv, mg, p, tab, st); break;
+    case 2: e = bwd_nw<2>(mq, mk, mv, mg, p, tab, st); break;
+    case 3: e = bwd_nw<3>(mq, mk, mv, mg, p, tab, st); break;
+    case 4: e = bwd_nw<4>(mq, mk, mv, mg, p, tab, st); break;
+    case 5: e = bwd_nw<5>(mq, mk, mv, mg, p, tab, st); break;
+    case 6: e = bwd_nw<6>(mq, mk, mv, mg, p, tab, st); break;
+    case 7: e = bwd_nw<7>(mq, mk, mv, mg, p, tab, st); break;
+    default: e = bwd_nw<8>(mq, mk, mv, mg, p, tab, st); break;
+  }
   return e == cudaSuccess ? 1 : -1;
 }
 
