@@ -47,9 +47,16 @@ def build_oracle():
     _run(["make", "-s", "-C", os.path.join(ROOT, "oracle")])
 
 
+def build_cpp_tests():
+    """tests/cpp: the C++ adapter and the drop-in check binaries (needs the
+    reference headers, so only where /root/reference exists)."""
+    _run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")])
+
+
 def build_all(force=False):
     build_cuda(force=force)
     build_oracle()
+    build_cpp_tests()
 
 
 if __name__ == "__main__":
