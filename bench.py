@@ -286,7 +286,8 @@ def run_ours(args, world, rank, local):
             with open(traffic) as f:
                 tr = json.load(f).get(args.workload)
             if tr:
-                res["roofline"]["traffic"] = tr
+                res["roofline"]["traffic"] = tr.get("bwd")
+                res["roofline"]["traffic_source"] = "profiles/traffic.json (ncu, per launch)"
         except Exception:
             pass
 
