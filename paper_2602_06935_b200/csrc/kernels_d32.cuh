@@ -149,8 +149,10 @@ __device__ __forceinline__ void normalize_rows(uint8_t* X, int r0, int N, const 
     ss += __shfl_xor_sync(0xffffffffu, ss, 4);
     if (r < N) {
       const bool valid = flag == nullptr || flag[r] != 0;
-      const float nrm = sqrtf(ss + eps);
-      const float iv = 1.0f / nrm;
+      // MUFU.RSQ (<= 2 ulp): the IEEE sqrt + divide sequences cost ~25
+      // instructions per row group and 10 KB of code, for no visible accuracy
+      const float iv = rsqrtf(ss + eps);
+      const float nrm = (ss + eps) * iv;
       x = valid ? make_float4(x.x * iv, x.y * iv, x.z * iv, x.w * iv)
                 : make_float4(0.f, 0.f, 0.f, 0.f);
       st4(a, x);
@@ -169,7 +171,7 @@ __device__ __forceinline__ void row_reduce(const uint8_t* X, const uint8_t* Y, i
   const int ag = lane >> 3, bg = lane & 7;
   const uint8_t* xb = X + r0 * kRowBytes;
   const uint8_t* yb = Y + r0 * kRowBytes;
-#pragma unroll
+#pragma unroll 1
   for (int t = 0; t < 4; ++t) {
     if (r0 + 8 * t >= N) break;  // warp-uniform
 #pragma unroll
@@ -212,7 +214,9 @@ __device__ __forceinline__ void row_output(const uint8_t* X, const float* M, int
     for (int p = 0; p < 4; ++p) o[j][p] = f2(0.f, 0.f);
   const uint8_t* xb = X + (r0 + rg) * kRowBytes;
   const float* mb = M + 4 * cg;
-#pragma unroll
+  // Not unrolled over c: the fully unrolled form (650 SASS instructions per
+  // call site, ~100 KB for the backward) thrashed the instruction cache.
+#pragma unroll 1
   for (int c = 0; c < 8; ++c) {
     const uint8_t* xc = xb + ((c ^ rg) << 4);  // (r & 7) == rg for all four rows
     float4 xv[4];
@@ -526,8 +530,9 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_fwd_d32_kernel(
 #pragma unroll
       for (int x = 0; x < 8; ++x) ss = fmaf(qv[x], qv[x], ss);
       ss = row_sum4(ss);
-      const float nrm = sqrtf(ss + eps);
-      const float w = scale * (1.0f / nrm);
+      const float iv = rsqrtf(ss + eps);
+      const float nrm = (ss + eps) * iv;
+      const float w = scale * iv;
       if (r < N) {
         float v[8];
         unpack(o[j], v);
