@@ -188,17 +188,18 @@ def run_ours(args, world, rank, local):
     dm_tot = torch.zeros(layers, dtype=torch.float64, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     m = 1.0
+    flags = _lib.FLAG_FP32_PIPE if args.path == "fp32pipe" else 0
 
     launches = [0]
 
     def fwd(t):
         ops.forward(t["q"], t["k"], t["v"], t["valid"], m, out=t["out"], saved_S=t["S"],
-                    stream=stream)
+                    stream=stream, flags=flags)
         launches[0] += _lib.launches()
 
     def bwd(t, i):
         ops.backward(t["q"], t["k"], t["v"], t["valid"], m, t["d_out"], t["S"], t["dq"],
-                     t["dk"], t["dv"], t["dm_unit"], dm_tot[i:i + 1], stream=stream)
+                     t["dk"], t["dv"], t["dm_unit"], dm_tot[i:i + 1], stream=stream, flags=flags)
         launches[0] += _lib.launches()
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -268,6 +269,7 @@ def run_ours(args, world, rank, local):
         "config": {"workload": desc, "name": args.workload, "global_batch": global_b,
                    "batch_per_gpu": B, "seq_len": N, "heads": H, "head_dim": D, "model_dim": H * D,
                    "layers": layers, "parallelism": f"dp{world} (batch x head shards)",
+                   "kernel_path": args.path,
                    "l2": "flushed between timed steps (256 MiB write), outside the events"},
         "roofline": {"bound": "hbm", "kernel": "cos_bwd (backward, dominant)",
                      "achieved": bwd_gbs, "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak,
@@ -451,6 +453,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ml1m", choices=sorted(WORKLOADS))
+    ap.add_argument("--path", default="tcgen05", choices=["tcgen05", "fp32pipe"],
+                    help="d_h=32 kernels: tcgen05 3xTF32 (default) or the FP32-pipe variant")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -64,6 +64,7 @@ extern "C" {
 
 /* Kernel-path selection (cotten_desc.flags); default 0 = fastest available. */
 #define COTTEN_FLAG_FORCE_GENERIC 1 /* always use the generic-D kernels */
+#define COTTEN_FLAG_FP32_PIPE 2     /* d_h = 32 fp32: FP32-pipe kernels instead of tcgen05 */
 
 typedef struct cotten_desc {
   int64_t batch;     /* B  sequences                       */

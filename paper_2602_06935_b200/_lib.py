@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcotten.so")
+# COTTEN_LIB overrides the in-tree library (A/B builds of kernel variants).
+LIB_PATH = os.environ.get("COTTEN_LIB") or os.path.join(_HERE, "libcotten.so")
 
 COTTEN_OK = 0
 COTTEN_ERR_INTERNAL = 1
@@ -20,6 +21,7 @@ F32, BF16, F64 = 0, 1, 2
 DTYPES = {"f32": F32, "float32": F32, "bf16": BF16, "bfloat16": BF16, "f64": F64, "float64": F64}
 
 FLAG_FORCE_GENERIC = 1
+FLAG_FP32_PIPE = 2  # d_h=32 fp32: the FP32-pipe kernels instead of the tcgen05 ones
 STATUS_EMPTY_SEQUENCE = 1
 
 

@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels_d32.cuh"
 #include "kernels_generic.cuh"
+#include "kernels_tc.cuh"
 
 namespace cotten {
 namespace {
@@ -180,7 +181,13 @@ thread_local Scratch g_dm_scratch, g_s_scratch, g_g_scratch;
 template <typename T>
 void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
-  if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && fast_fwd_supported<T>(p)) {
+  const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
+  if (tensor && tc_fwd_supported<T>(p)) {
+    const int n = launch_tc_fwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: tensor-core forward launch failed"};
+    g_launches += n;
+  } else if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && fast_fwd_supported<T>(p)) {
     const int n = launch_fast_fwd<T>(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fast forward launch failed (tensor map)"};
@@ -199,7 +206,13 @@ void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
 template <typename T>
 void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
-  if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && fast_bwd_supported<T>(p)) {
+  const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
+  if (tensor && tc_bwd_supported<T>(p)) {
+    const int n = launch_tc_bwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: tensor-core backward launch failed"};
+    g_launches += n;
+  } else if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && fast_bwd_supported<T>(p)) {
     const int n = launch_fast_bwd<T>(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fast backward launch failed (tensor map)"};

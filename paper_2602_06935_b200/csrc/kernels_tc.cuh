@@ -1,0 +1,1124 @@
+// Tensor-core (tcgen05 / TMEM) cosine-attention kernels for head_dim 32, fp32,
+// any seq_len up to 16384 — the B200 hot path for the ML-1M / ML-20M / Beauty
+// shapes and the d_h = 32 long-sequence sweep.
+//
+// Every unit (sequence b, head h) is streamed as 128-row chunks (one TMA box
+// of 128 rows x 128 B, 128-byte swizzle, rows past N zero-filled by TMA):
+//   forward   pass 1 over (K, V) chunks: S = K~^T V   (reduction over rows)
+//             pass 2 over  Q     chunks: O = s Q~ S   (row output)
+//   backward  pass 1 over (Q, dO) chunks: G = Q~^T dO, dQ~ = s dO S^T
+//             pass 2 over (K, V)  chunks: dV = K~ dA,  dK~ = V dA^T   (dA = s G)
+// (attention.cpp:297-395 and :397-441).  All six contractions run on the
+// tensor cores as 3xTF32: every operand x is split by the worker threads
+// into hi = x rounded to tf32 (low 13 mantissa bits clear) and lo = x - hi
+// (exact in fp32), and the MMAs accumulate hi*hi + hi*lo + lo*hi
+// (+ lo*lo for the reductions, which is free there) in fp32 TMEM — within
+// ~1e-6 of fp32, well inside the 1e-5 bar, where plain TF32 is at ~4e-4.
+//
+//   * reductions (S, G): tcgen05.mma M=64, N=64, K=8 rows per instruction,
+//     A and B both MN-major straight from the TMA tiles: A's two 32-wide
+//     M atoms are [x_hi | x_lo] and B's two N atoms are [y_hi | y_lo], so one
+//     instruction accumulates all four hi/lo products of 8 rows into TMEM;
+//   * row outputs (O, dQ~, dV, dK~): M=128 rows, N=32, K=32 (4 k-steps x 3
+//     products), A = the chunk (K-major SW128), B = the 32x32 state operand
+//     (S, S^T, dA or dA^T, split hi/lo) written by the workers.
+//
+// Warp roles (352 threads, one CTA per SM, persistent over units):
+//   warps 0-7  two worker groups of 4 warps; group g takes chunks i = g (mod 2)
+//              and thread t owns row t of its chunk (= TMEM lane t): row norms,
+//              masking, hi/lo split (hi in place in the TMA stage, lo into the
+//              group's lo buffer), then the epilogue: TMEM -> registers ->
+//              scale / Jacobian / mask -> the chunk's own TMA stage as staging
+//              -> TMA store.  While one group waits on its MMAs the other
+//              splits or stores, so each SMSP always has a worker to issue.
+//   warp 8     TMA producer: raw chunks into a 4-stage ring.
+//   warp 9     MMA issuer (one elected thread) + TMEM allocator.
+//   warp 10    mask warp: up to two units ahead, valid bytes -> bitmask,
+//              true_n, s = exp(-m ln n), coef = -ln(n) s in fp64
+//              (attention.cpp:303-304, :402-408).
+// Nothing but the outputs, S (4 KB per unit) and dm reach HBM.
+#pragma once
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels_d32.cuh"
+
+namespace cotten {
+namespace tc {
+
+using d32::mbar_arrive;
+using d32::mbar_expect_tx;
+using d32::mbar_init;
+using d32::mbar_wait;
+using d32::smem_u32;
+using d32::tma_load_4d;
+
+constexpr int kRows = 128;                 // rows per chunk
+constexpr uint32_t kTile = 16384;          // 128 rows x 128 B
+constexpr uint32_t kStage = 2 * kTile;     // two tensors per chunk
+constexpr int kRaw = 4;                    // TMA stages
+constexpr int kMaxN = 16384;               // flag bitmask capacity
+constexpr int kGroups = 2;                 // worker groups (alternate chunks)
+constexpr int kWorkerWarps = 4 * kGroups;
+constexpr int kWarpProducer = kWorkerWarps;
+constexpr int kWarpMma = kWorkerWarps + 1;
+constexpr int kWarpMask = kWorkerWarps + 2;
+constexpr int kThreads = (kWorkerWarps + 3) * 32;
+
+// Shared-memory plan (bytes; every operand region 1024-aligned for SW128).
+constexpr uint32_t kOffRaw = 0;
+constexpr uint32_t kOffLo = kOffRaw + kRaw * kStage;       // 2 lo buffers
+constexpr uint32_t kOffOps = kOffLo + 2 * kStage;          // 6 x 4 KB state operands
+constexpr uint32_t kOffFlags = kOffOps + 6 * 4096;         // 2 x 2 KB bitmasks
+constexpr uint32_t kOffMisc = kOffFlags + 2 * (kMaxN / 8);  // 2 x 16 B unit constants, tmem base
+constexpr uint32_t kOffBar = kOffMisc + 64;
+constexpr uint32_t kSmemBytes = kOffBar + 32 * 8;
+// state operands (32 rows x 128 B each): 0/1 = S-side hi/lo, 2/3 = dA rows hi/lo,
+// 4/5 = dA^T rows hi/lo
+constexpr uint32_t kOpBytes = 4096;
+
+// TMEM: 512 columns.  Backward: [0, 64) G; group g's buffer at kBwdBuf0 + 192 g:
+// pass 1 [+0, +32) dQ~, [+64, +128) dO hi/lo A operand;
+// pass 2 [+0, +32) dV, [+32, +64) dK~, [+64, +128) K~ hi/lo, [+128, +192) V hi/lo.
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kBwdBuf0 = 64;
+constexpr uint32_t kBwdBufCols = 192;
+// Forward: [0, 64) S; group g's buffer at kFwdBuf0 + 96 g: [+0, +32) O,
+// [+32, +96) Q~ hi/lo A operand.
+constexpr uint32_t kFwdBuf0 = 64;
+constexpr uint32_t kFwdBufCols = 96;
+
+struct UnitConst {  // per flag slot, written by the mask warp
+  int tn;
+  float s;
+  double coef;
+};
+
+// ---- tcgen05 / TMA-store PTX ------------------------------------------------
+
+// One lane of a converged warp (the MMA issuer runs the whole warp through
+// its loop so that descriptors stay in uniform registers and no per-MMA
+// uniformity loop is generated around a diverged single-lane issue).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P1;\nelect.sync _|P1, 0xffffffff;\nselp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// Shared-memory matrix descriptor (sm_100 version bits).  layout 2 =
+// SWIZZLE_128B (16-byte granules, K-major operands); layout 1 =
+// SWIZZLE_128B_BASE32B (32-byte granules) — the only MN-major layout tf32
+// accepts (measured: scripts/dev/mma_probe3.cu).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                          uint32_t layout = 2) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&r)[32]) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(r);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+        "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+        "=r"(u[14]), "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]),
+        "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]),
+        "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+      : "r"(taddr));
+}
+// A operand rows into TMEM: lane = this thread's row, 32 consecutive columns.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&r)[32]) {
+  const uint32_t* u = reinterpret_cast<const uint32_t*>(r);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]),
+      "r"(u[8]), "r"(u[9]), "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]),
+      "r"(u[15]), "r"(u[16]), "r"(u[17]), "r"(u[18]), "r"(u[19]), "r"(u[20]), "r"(u[21]),
+      "r"(u[22]), "r"(u[23]), "r"(u[24]), "r"(u[25]), "r"(u[26]), "r"(u[27]), "r"(u[28]),
+      "r"(u[29]), "r"(u[30]), "r"(u[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// D (TMEM) += A (TMEM, K-major: lane = row, column = k) * B (smem descriptor).
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b,
+                                            uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---- row access in a 128B-swizzled 128-row tile -----------------------------
+
+__device__ __forceinline__ uint32_t chunk_off(int row, int j) {
+  return (uint32_t)row * 128u + ((uint32_t)(j ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ void load_row(const uint8_t* tile, int row, float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = *reinterpret_cast<const float4*>(tile + chunk_off(row, j));
+    x[4 * j] = v.x;
+    x[4 * j + 1] = v.y;
+    x[4 * j + 2] = v.z;
+    x[4 * j + 3] = v.w;
+  }
+}
+__device__ __forceinline__ void store_row(uint8_t* tile, int row, const float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(tile + chunk_off(row, j)) =
+        make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+}
+// Same for the 32-byte-granule swizzle (TMA SWIZZLE_128B_ATOM_32B): 32-byte
+// granule g of row r sits at granule g ^ (r & 3).
+__device__ __forceinline__ uint32_t chunk_off32(int row, int j) {
+  return (uint32_t)row * 128u + ((uint32_t)((j >> 1) ^ (row & 3)) << 5) + ((uint32_t)(j & 1) << 4);
+}
+__device__ __forceinline__ void load_row32(const uint8_t* tile, int row, float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = *reinterpret_cast<const float4*>(tile + chunk_off32(row, j));
+    x[4 * j] = v.x;
+    x[4 * j + 1] = v.y;
+    x[4 * j + 2] = v.z;
+    x[4 * j + 3] = v.w;
+  }
+}
+// Round to the nearest tf32 (ties away from zero): exact in tf32, so the
+// tensor core reads it unchanged.  Operands are split x = hi + lo with
+// hi = tf32(x), |x - hi| <= 2^-11 |x|, and lo = tf32(x - hi), so what the
+// MMAs see differs from x by at most 2^-22 |x|.
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+#ifndef COTTEN_TC_ROUND_LO
+#define COTTEN_TC_ROUND_LO 0
+#endif
+__device__ __forceinline__ float tf32_lo(float x, float hi) {
+#if COTTEN_TC_ROUND_LO
+  return tf32_hi(x - hi);
+#else
+  return x - hi;
+#endif
+}
+// hi in place of the TMA tile, lo into the lo buffer.
+__device__ __forceinline__ void store_split(uint8_t* hi_tile, uint8_t* lo_tile, int row,
+                                            const float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      h[e] = tf32_hi(x[4 * j + e]);
+      l[e] = tf32_lo(x[4 * j + e], h[e]);
+    }
+    *reinterpret_cast<float4*>(hi_tile + chunk_off(row, j)) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(lo_tile + chunk_off(row, j)) = make_float4(l[0], l[1], l[2], l[3]);
+  }
+}
+__device__ __forceinline__ void store_split32(uint8_t* hi_tile, uint8_t* lo_tile, int row,
+                                              const float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      h[e] = tf32_hi(x[4 * j + e]);
+      l[e] = tf32_lo(x[4 * j + e], h[e]);
+    }
+    *reinterpret_cast<float4*>(hi_tile + chunk_off32(row, j)) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(lo_tile + chunk_off32(row, j)) = make_float4(l[0], l[1], l[2], l[3]);
+  }
+}
+__device__ __forceinline__ float sumsq(const float (&x)[32]) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    a0 = fmaf(x[k], x[k], a0);
+    a1 = fmaf(x[k + 1], x[k + 1], a1);
+    a2 = fmaf(x[k + 2], x[k + 2], a2);
+    a3 = fmaf(x[k + 3], x[k + 3], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+__device__ __forceinline__ float dot32(const float (&x)[32], const float (&y)[32]) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    a0 = fmaf(x[k], y[k], a0);
+    a1 = fmaf(x[k + 1], y[k + 1], a1);
+    a2 = fmaf(x[k + 2], y[k + 2], a2);
+    a3 = fmaf(x[k + 3], y[k + 3], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+// Element (n, k) of a 32-row operand buffer (row n, column k).
+__device__ __forceinline__ uint32_t elem_off(int n, int k) {
+  return chunk_off(n, k >> 2) + (uint32_t)(k & 3) * 4u;
+}
+
+__device__ __forceinline__ bool flag_at(const uint32_t* fl, int r) {
+  return (fl[r >> 5] >> (r & 31)) & 1u;
+}
+
+// ---- the mask warp ------------------------------------------------------------
+
+// Bitmask of valid rows + true_n + the fp64 scale constants of unit (b).
+__device__ __forceinline__ void mask_unit(const OpParams& p, int64_t b, uint32_t* fl,
+                                          UnitConst* uc, int lane) {
+  const int N = (int)p.N;
+  const int words = (N + 31) >> 5;
+  int cnt = 0;
+  const uint8_t* row = p.valid ? p.valid + b * p.msb : nullptr;
+  for (int w0 = 0; w0 < words; w0 += 8) {
+    uint8_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // 8 loads in flight before the first ballot
+      const int r = (w0 + k) * 32 + lane;
+      v[k] = (w0 + k < words && r < N) ? (row ? __ldg(row + r) : (uint8_t)1) : (uint8_t)0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, v[k] != 0);
+      if (w0 + k < words) {
+        if (lane == 0) fl[w0 + k] = bits;
+        cnt += __popc(bits);
+      }
+    }
+  }
+  if (lane == 0) {
+    UnitConst c;
+    c.tn = cnt;
+    if (cnt > 0) {
+      const double ln = log((double)cnt);
+      const double s = exp(-p.m * ln);  // attention.cpp:304 / :403, fp64
+      c.s = (float)s;
+      c.coef = -ln * (double)c.s;  // attention.cpp:408
+    } else {  // UsageError in the reference (attention.cpp:44): NaN outputs + status bit
+      c.s = __int_as_float(0x7fc00000);
+      c.coef = __longlong_as_double(0x7ff8000000000000ll);
+      if (p.status) atomicOr(p.status, 1);
+    }
+    *uc = c;
+  }
+}
+
+// ---- MMA issue helpers (one thread) ----------------------------------------------
+
+// Reduction R += x^T y over the valid 8-row groups of a chunk (tiles in the
+// 32-byte-granule swizzle): x's hi tile at xh, lo at xh + lbo; y's hi at yh,
+// lo at yh + lbo.  D (M=64 x N=64) rows 0-31 are x_hi, 32-63 x_lo; columns
+// 0-31 y_hi, 32-63 y_lo.  SBO = 512: 4-row groups of the 32B-granule atom.
+__device__ __forceinline__ void issue_reduction(uint32_t d, uint32_t xh, uint32_t yh,
+                                                uint32_t lbo, int ksteps, bool first) {
+  const uint32_t id = idesc_tf32(64, 64, true, true);
+  for (int kk = 0; kk < ksteps; ++kk)
+    mma_tf32(d, sdesc(xh + 1024u * kk, lbo, 512u, 1u), sdesc(yh + 1024u * kk, lbo, 512u, 1u), id,
+             (first && kk == 0) ? 0u : 1u);
+}
+// Row output D = A B with A = this chunk's 128 rows in TMEM (K-major: lane =
+// row, hi at columns [ah, ah+32), lo at [ah+32, ah+64)) and B = a 32-row
+// state operand in shared memory (hi at bh, lo at bl): 3xTF32 = 12 MMAs of
+// M=128, N=32, K=8.  A from TMEM keeps these small-N MMAs off the shared-
+// memory port (an SS MMA would re-read its 4 KB A tile for every 16-cycle
+// instruction).
+__device__ __forceinline__ void issue_rowout_ts(uint32_t d, uint32_t ah, uint32_t bh, uint32_t bl) {
+  const uint32_t id = idesc_tf32(128, 32, false, false);
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const uint32_t o = 32u * kk;
+    mma_tf32_ts(d, ah + 8 * kk, sdesc(bh + o, 16u, 1024u), id, kk > 0 ? 1u : 0u);
+    mma_tf32_ts(d, ah + 8 * kk, sdesc(bl + o, 16u, 1024u), id, 1u);
+    mma_tf32_ts(d, ah + 32 + 8 * kk, sdesc(bh + o, 16u, 1024u), id, 1u);
+  }
+}
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&r)[32]) {
+  tmem_ld32(taddr, r);
+  tmem_wait_ld();
+}
+// Split a row into hi / lo and store both as TMEM A-operand columns of this
+// thread's lane: hi at [col, col+32), lo at [col+32, col+64).
+__device__ __forceinline__ void tmem_store_split(uint32_t taddr, const float (&x)[32]) {
+  float h[32], l[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    h[k] = tf32_hi(x[k]);
+    l[k] = tf32_lo(x[k], h[k]);
+  }
+  tmem_st32(taddr, h);
+  tmem_st32(taddr + 32, l);
+}
+
+// ---- optional phase trace (debug builds: -DCOTTEN_TC_TRACE=1) ---------------------
+// Thread 0 of each worker group stamps clock64() at 5 points of its first
+// kTraceItems items: [0] before the TMA wait, [1] data landed, [2] split
+// published, [3] MMAs done, [4] epilogue issued; the MMA thread (slot 2) stamps
+// [0] before its split wait, [1] after it, [2] after issuing, per item.
+// Layout [cta][3][item][8].
+#ifndef COTTEN_TC_TRACE
+#define COTTEN_TC_TRACE 0
+#endif
+constexpr int kTraceItems = 64;
+#if COTTEN_TC_TRACE
+#define TC_TRACE(k)                                                                       \
+  do {                                                                                    \
+    if (t == 0 && p.workspace && n_tr < kTraceItems)                                     \
+      static_cast<long long*>(p.workspace)[((blockIdx.x * 3 + g) * kTraceItems + n_tr) * 8 + (k)] = \
+          clock64();                                                                      \
+  } while (0)
+#define TC_TRACE_MMA(k)                                                                   \
+  do {                                                                                    \
+    if (lane == 0 && p.workspace && it < kTraceItems)                                     \
+      static_cast<long long*>(p.workspace)[((blockIdx.x * 3 + 2) * kTraceItems + it) * 8 + (k)] = \
+          clock64();                                                                      \
+  } while (0)
+#else
+#define TC_TRACE(k) \
+  do {              \
+  } while (0)
+#define TC_TRACE_MMA(k) \
+  do {                  \
+  } while (0)
+#endif
+
+// ---- warp roles, barriers -------------------------------------------------------
+
+struct Bars {
+  uint64_t raw_full[4], raw_empty[4];  // producer <-> workers (stage = item & 3)
+  uint64_t split_full[2], mma_done[2];  // workers <-> MMA issuer (group = item & 1)
+  uint64_t op_ready;                    // state operand (S or dA) written, per unit
+  uint64_t fl_full[2], fl_empty[2];     // mask warp <-> workers (slot = unit & 1)
+};
+static_assert(sizeof(Bars) <= 256, "barrier area");
+
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+}
+
+// Barrier init + TMEM allocation (256 columns, one CTA per SM).
+__device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* tslot, int warp) {
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&br->raw_full[i], 1);
+      mbar_init(&br->raw_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&br->split_full[i], 4);
+      mbar_init(&br->mma_done[i], 1);
+      mbar_init(&br->fl_full[i], 1);
+      mbar_init(&br->fl_empty[i], kWorkerWarps);
+    }
+    mbar_init(&br->op_ready, 1);
+    d32::fence_barrier_init();
+  }
+  if (warp == kWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_u32(tslot)), "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  return *tslot;
+}
+__device__ __forceinline__ void tc_teardown(uint32_t tmem, int warp) {
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpMma) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  }
+}
+
+// The mask warp: one unit at a time, up to two units ahead of the workers.
+__device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars* br, int lane) {
+  UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
+  const int units = (int)(p.B * p.H), H = (int)p.H;
+  int j = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+    const int sl = j & 1;
+    mbar_wait(&br->fl_empty[sl], ((j >> 1) & 1) ^ 1);
+    mask_unit(p, u / H, reinterpret_cast<uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8)),
+              &ucs[sl], lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&br->fl_full[sl]);
+  }
+}
+
+// ---- reduction epilogue (S or G) --------------------------------------------------
+// D (M=64 layout: row m at lane (m%16) + 32(m/16)) -> full 32x32 row a = 16 wq + l
+// in the group's warps wq < 2, lanes < 16.  scratch: 4 KB of free smem.
+__device__ __forceinline__ bool reduce_rows(uint32_t tmem, uint8_t* scratch, int wq, int lane,
+                                            int g, float (&row)[32]) {
+  float a[32], c[32];
+  const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16);
+  tmem_ld32(ta, a);
+  tmem_ld32(ta + 32, c);
+  tmem_wait_ld();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) row[k] = a[k] + c[k];  // x.. y_hi + x.. y_lo
+  const int ra = 16 * (wq & 1) + lane;               // row a held by this lane
+  if (wq >= 2 && lane < 16) store_row(scratch, ra, row);
+  group_sync(g);
+  const bool own = wq < 2 && lane < 16;
+  if (own) {
+    float o[32];
+    load_row(scratch, ra, o);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) row[k] += o[k];  // + x_lo y
+  }
+  return own;
+}
+
+// hi / lo split of a row into two register arrays.
+__device__ __forceinline__ void split_regs(const float (&x)[32], float (&h)[32], float (&l)[32]) {
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    h[k] = tf32_hi(x[k]);
+    l[k] = tf32_lo(x[k], h[k]);
+  }
+}
+__device__ __forceinline__ void store_row32(uint8_t* tile, int row, const float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(tile + chunk_off32(row, j)) =
+        make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+}
+
+// Release the raw stage of this group's previous item once its TMA store (if
+// any) has finished reading it.
+__device__ __forceinline__ void release_prev(Bars* br, int& prev_st, int t) {
+  if (prev_st >= 0 && t == 0) {
+    bulk_wait_read0();
+    mbar_arrive(&br->raw_empty[prev_st]);
+  }
+}
+
+// ======================================================================================
+// Forward
+// ======================================================================================
+__global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
+    const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
+    const OpParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int N = (int)p.N, H = (int)p.H;
+  const int units = (int)(p.B * p.H);
+  const int C = (N + kRows - 1) / kRows;
+  // pass 2 (Q) only when O or the Q norms are wanted (an S-only forward
+  // feeds a backward that was given no saved state)
+  const int P = (p.out != nullptr || p.saved_norms != nullptr) ? 2 : 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
+  UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
+  uint8_t* ops = smem + kOffOps;
+  const uint32_t tmem = tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
+
+  if (warp == kWarpProducer) {  // ===== TMA: (K, V) chunks then Q chunks =====
+    if (lane == 0) {
+      d32::prefetch_map(&tk);
+      d32::prefetch_map(&tv);
+      d32::prefetch_map(&tq);
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int ps = 0; ps < P; ++ps)
+          for (int c = 0; c < C; ++c, ++it) {
+            const int st = it & 3;
+            mbar_wait(&br->raw_empty[st], ((it >> 2) & 1) ^ 1);
+            uint8_t* dst = smem + kOffRaw + st * kStage;
+            if (ps == 0) {
+              mbar_expect_tx(&br->raw_full[st], 2 * kTile);
+              tma_load_4d(dst, &tk, 0, c * kRows, h, b, &br->raw_full[st]);
+              tma_load_4d(dst + kTile, &tv, 0, c * kRows, h, b, &br->raw_full[st]);
+            } else {
+              mbar_expect_tx(&br->raw_full[st], kTile);
+              tma_load_4d(dst, &tq, 0, c * kRows, h, b, &br->raw_full[st]);
+            }
+          }
+      }
+    }
+  } else if (warp == kWarpMma) {  // ===== MMA issuer (whole warp, one elected lane issues) =====
+    int it = 0, j = 0;
+    const uint32_t base = smem_u32(smem);
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      for (int ps = 0; ps < P; ++ps)
+        for (int c = 0; c < C; ++c, ++it) {
+          const int st = it & 3, g = it & 1;
+          TC_TRACE_MMA(0);
+          mbar_wait(&br->split_full[g], (it >> 1) & 1);
+          if (ps == 0 && c == 0 && P == 1 && j > 0)  // previous S read before it is overwritten
+            mbar_wait(&br->op_ready, (j - 1) & 1);
+          if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
+          tc_fence_after();
+          TC_TRACE_MMA(1);
+          const uint32_t X = base + kOffRaw + st * kStage;
+          const uint32_t Y = base + kOffLo + g * kStage;
+          if (elect_one()) {
+            if (ps == 0) {  // S += K~^T V (attention.cpp:345-353)
+              const int rows = min(kRows, N - c * kRows);
+              issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c == 0);
+            } else {  // O = Q~ S (attention.cpp:379-387); B row n = S column n
+              const uint32_t D = tmem + kFwdBuf0 + kFwdBufCols * g;
+              issue_rowout_ts(D, D + 32, base + kOffOps, base + kOffOps + kOpBytes);
+            }
+            TC_TRACE_MMA(2);
+            mma_commit(&br->mma_done[g]);
+          }
+          __syncwarp();
+        }
+    }
+  } else if (warp == kWarpMask) {
+    mask_loop(p, smem, br, lane);
+  } else {  // ===== workers: group g takes items it = g (mod 2); thread t owns chunk row t =====
+    const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
+    const float eps = (float)p.eps;
+    float* O = static_cast<float*>(p.out);
+    float* norms_all = static_cast<float*>(p.saved_norms);
+    float* gS_all = static_cast<float*>(p.saved_S);
+    const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
+    int it = 0, j = 0, prev_st = -1, n_tr = 0;
+    (void)n_tr;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int b = u / H, h = u - b * H;
+      const int sl = j & 1;
+      const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
+      float* norms = norms_all ? norms_all + (int64_t)u * 2 * N : nullptr;
+      mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
+      const UnitConst uc = ucs[sl];
+      for (int ps = 0; ps < P; ++ps)
+        for (int c = 0; c < C; ++c, ++it) {
+          if ((it & 1) != g) continue;
+          const int st = it & 3;
+          const int r = c * kRows + t;
+          uint8_t* X = smem + kOffRaw + st * kStage;
+          uint8_t* Y = smem + kOffLo + g * kStage;
+          TC_TRACE(0);
+          mbar_wait(&br->raw_full[st], (it >> 2) & 1);
+          TC_TRACE(1);
+          if (ps == 0) {  // K~ (masked, attention.cpp:334-343) and V, 32-byte-granule tiles
+            float kx[32], vx[32];
+            load_row32(X, t, kx);
+            load_row32(X + kTile, t, vx);
+            const bool f = r < N && flag_at(fl, r);
+            const float ss = sumsq(kx) + eps;
+            const float iv = rsqrtf(ss);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) kx[k] = f ? kx[k] * iv : 0.f;  // selected: NaN-safe
+            if (norms && r < N) norms[N + r] = f ? ss * iv : 1.0f;  // :336, :343
+            release_prev(br, prev_st, t);
+            store_split32(X, Y, t, kx);
+            store_split32(X + kTile, Y + kTile, t, vx);
+          } else {  // Q~ for every row (attention.cpp:366-377)
+            float qx[32];
+            load_row(X, t, qx);
+            const float ss = sumsq(qx) + eps;
+            const float iv = rsqrtf(ss);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) qx[k] *= iv;
+            if (norms && r < N) norms[r] = ss * iv;
+            release_prev(br, prev_st, t);
+            tmem_store_split(tmem + kFwdBuf0 + kFwdBufCols * g + 32 + lane_base, qx);
+            tmem_wait_st();
+            tc_fence_before();
+          }
+          prev_st = st;
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&br->split_full[g]);
+          TC_TRACE(2);
+
+          // ---- epilogue of this item ----
+          mbar_wait(&br->mma_done[g], (it >> 1) & 1);
+          tc_fence_after();
+          TC_TRACE(3);
+          if (ps == 0) {
+            if (c == C - 1) {  // S complete: saved S + the O operand (row n = S column n)
+              float row[32];
+              const bool own = reduce_rows(tmem, Y + kTile, wq, lane, g, row);
+              if (own) {
+                const int a = 16 * wq + lane;
+                if (gS_all) {
+                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024 + a * 32);
+#pragma unroll
+                  for (int q = 0; q < 8; ++q)
+                    gs[q] = make_float4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
+                }
+#pragma unroll
+                for (int n = 0; n < 32; ++n) {
+                  const float hv = tf32_hi(row[n]);
+                  *reinterpret_cast<float*>(ops + elem_off(n, a)) = hv;
+                  *reinterpret_cast<float*>(ops + kOpBytes + elem_off(n, a)) = tf32_lo(row[n], hv);
+                }
+              }
+              fence_proxy_async();
+              tc_fence_before();
+              group_sync(g);
+              if (t == 0) mbar_arrive(&br->op_ready);
+            }
+          } else {  // O rows = s (Q~ S) (attention.cpp:379-387), staged in the raw stage
+            float acc[32];
+            tmem_ld_row(tmem + kFwdBuf0 + kFwdBufCols * g + lane_base, acc);
+            tc_fence_before();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) acc[k] *= uc.s;
+            store_row(X, t, acc);
+            fence_proxy_async();
+            group_sync(g);
+            if (t == 0 && O) tma_store_4d(&to, X, 0, c * kRows, h, b);
+          }
+          TC_TRACE(4);
+          ++n_tr;
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
+    }
+    if (t == 0) bulk_wait0();
+  }
+  tc_teardown(tmem, warp);
+}
+
+// ======================================================================================
+// Backward
+// ======================================================================================
+__global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
+    const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+    const __grid_constant__ CUtensorMap tdq, const __grid_constant__ CUtensorMap tdk,
+    const __grid_constant__ CUtensorMap tdv, const OpParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int N = (int)p.N, H = (int)p.H;
+  const int units = (int)(p.B * p.H);
+  const int C = (N + kRows - 1) / kRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
+  UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
+  double* dm_x = reinterpret_cast<double*>(smem + kOffMisc + 40);
+  uint8_t* ops = smem + kOffOps;
+  const uint32_t tmem = tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
+
+  if (warp == kWarpProducer) {  // ===== TMA: (Q, dO) chunks, then (K, V) chunks =====
+    if (lane == 0) {
+      d32::prefetch_map(&tq);
+      d32::prefetch_map(&tdo);
+      d32::prefetch_map(&tk);
+      d32::prefetch_map(&tv);
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int ps = 0; ps < 2; ++ps)
+          for (int c = 0; c < C; ++c, ++it) {
+            const int st = it & 3;
+            mbar_wait(&br->raw_empty[st], ((it >> 2) & 1) ^ 1);
+            uint8_t* dst = smem + kOffRaw + st * kStage;
+            mbar_expect_tx(&br->raw_full[st], 2 * kTile);
+            tma_load_4d(dst, ps == 0 ? &tq : &tk, 0, c * kRows, h, b, &br->raw_full[st]);
+            tma_load_4d(dst + kTile, ps == 0 ? &tdo : &tv, 0, c * kRows, h, b, &br->raw_full[st]);
+          }
+      }
+    }
+  } else if (warp == kWarpMma) {  // ===== MMA issuer (whole warp, one elected lane issues) =====
+    int it = 0, j = 0;
+    const uint32_t base = smem_u32(smem);
+    const uint32_t opS = base + kOffOps, opA = opS + 2 * kOpBytes, opAt = opS + 4 * kOpBytes;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      for (int ps = 0; ps < 2; ++ps)
+        for (int c = 0; c < C; ++c, ++it) {
+          const int st = it & 3, g = it & 1;
+          TC_TRACE_MMA(0);
+          mbar_wait(&br->split_full[g], (it >> 1) & 1);
+          if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
+          tc_fence_after();
+          TC_TRACE_MMA(1);
+          const uint32_t X = base + kOffRaw + st * kStage;
+          const uint32_t Y = base + kOffLo + g * kStage;
+          const uint32_t D = tmem + kBwdBuf0 + kBwdBufCols * g;
+          if (elect_one()) {
+            if (ps == 0) {
+              // G += Q~^T dO (attention.cpp:405)
+              const int rows = min(kRows, N - c * kRows);
+              issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c == 0);
+              // dQ~ (unscaled) = dO S^T (:410-411): A = dO hi/lo in TMEM, B row n = S row n
+              issue_rowout_ts(D, D + 64, opS, opS + kOpBytes);
+            } else {
+              // dV = K~ dA (:416): B row n = dA column n
+              issue_rowout_ts(D, D + 64, opAt, opAt + kOpBytes);
+              // dK~ = V dA^T (:415): B row n = dA row n
+              issue_rowout_ts(D + 32, D + 128, opA, opA + kOpBytes);
+            }
+            TC_TRACE_MMA(2);
+            mma_commit(&br->mma_done[g]);
+          }
+          __syncwarp();
+        }
+    }
+  } else if (warp == kWarpMask) {
+    mask_loop(p, smem, br, lane);
+  } else {  // ===== workers =====
+    const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
+    const float eps = (float)p.eps;
+    const float* gS_all = static_cast<const float*>(p.saved_S);
+    const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
+    // saved S of the group's next unit-start item, prefetched a unit ahead
+    // (group 0 always owns chunk 0 of pass 1: units have an even item count)
+    float4 snext[2];
+    auto fetch_S = [&](int u) {
+      if (u < units) {
+        const float4* gs = reinterpret_cast<const float4*>(gS_all + (int64_t)u * 1024);
+        snext[0] = __ldg(gs + t);
+        snext[1] = __ldg(gs + t + 128);
+      }
+    };
+    if (g == 0) fetch_S(blockIdx.x);
+    const float qnan = __int_as_float(0x7fc00000);
+    int it = 0, j = 0, prev_st = -1, n_tr = 0;
+    (void)n_tr;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int b = u / H, h = u - b * H;
+      const int sl = j & 1;
+      const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
+      mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
+      const UnitConst uc = ucs[sl];
+      for (int ps = 0; ps < 2; ++ps)
+        for (int c = 0; c < C; ++c, ++it) {
+          if ((it & 1) != g) continue;
+          const int st = it & 3;
+          const int r = c * kRows + t;
+          uint8_t* X = smem + kOffRaw + st * kStage;
+          uint8_t* Y = smem + kOffLo + g * kStage;
+          const uint32_t D = tmem + kBwdBuf0 + kBwdBufCols * g + lane_base;
+          TC_TRACE(0);
+          mbar_wait(&br->raw_full[st], (it >> 2) & 1);
+          TC_TRACE(1);
+          float xr[32], inv;
+          bool f = true;
+          if (ps == 0) {
+            // Q~ every row (:366-377, used again in :421-428); rows past N are exact
+            // zeros in G even for eps = 0.  Tiles use the 32-byte-granule swizzle.
+            float gy[32];
+            load_row32(X, t, xr);
+            load_row32(X + kTile, t, gy);
+            inv = rsqrtf(sumsq(xr) + eps);
+            const bool in = r < N;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) xr[k] = in ? xr[k] * inv : 0.f;
+            release_prev(br, prev_st, t);
+            store_split32(X, Y, t, xr);
+            float hv[32], lv[32];
+            split_regs(gy, hv, lv);
+            store_row32(X + kTile, t, hv);
+            store_row32(Y + kTile, t, lv);
+            tmem_st32(D + 64, hv);  // dO as the TMEM A operand of dQ~ = dO S^T
+            tmem_st32(D + 96, lv);
+            if (c == 0) {  // S rows (row n = S row n) for dQ~ = dO S^T
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2) {
+                const int e = t + 128 * e2;
+                const int n = e >> 3, q4 = e & 7;
+                const float4 v = snext[e2];
+                const float4 hq = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                *reinterpret_cast<float4*>(ops + chunk_off(n, q4)) = hq;
+                *reinterpret_cast<float4*>(ops + kOpBytes + chunk_off(n, q4)) =
+                    make_float4(tf32_lo(v.x, hq.x), tf32_lo(v.y, hq.y), tf32_lo(v.z, hq.z),
+                                tf32_lo(v.w, hq.w));
+              }
+              fetch_S(u + gridDim.x);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+          } else {  // K~ masked (:334-343), V as is
+            float vy[32];
+            load_row(X, t, xr);
+            load_row(X + kTile, t, vy);
+            f = r < N && flag_at(fl, r);
+            inv = rsqrtf(sumsq(xr) + eps);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) xr[k] = f ? xr[k] * inv : 0.f;  // selected: NaN-safe
+            release_prev(br, prev_st, t);
+            tmem_store_split(D + 64, xr);   // K~: A of dV = K~ dA
+            tmem_store_split(D + 128, vy);  // V:  A of dK~ = V dA^T
+            tmem_wait_st();
+            tc_fence_before();
+          }
+          prev_st = st;
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&br->split_full[g]);
+          TC_TRACE(2);
+
+          // ---- epilogue of this item ----
+          mbar_wait(&br->mma_done[g], (it >> 1) & 1);
+          tc_fence_after();
+          TC_TRACE(3);
+          if (ps == 0) {
+            // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428)
+            float gq[32];
+            tmem_ld_row(D, gq);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) gq[k] *= uc.s;
+            const float pr = dot32(gq, xr);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) gq[k] = (gq[k] - pr * xr[k]) * inv;
+            if (c == C - 1) {
+              // G complete: dm (:408), dA = s G (:412-413) as both state operands
+              float row[32];
+              const bool own = reduce_rows(tmem, Y + kTile, wq, lane, g, row);
+              double dot = 0.0;
+              if (own) {
+                const int a = 16 * wq + lane;
+                float sh[32], sl2[32];
+                load_row(ops, a, sh);
+                load_row(ops + kOpBytes, a, sl2);
+#pragma unroll
+                for (int k = 0; k < 32; k += 4) {
+                  float d = row[k] * (sh[k] + sl2[k]);
+                  d = fmaf(row[k + 1], sh[k + 1] + sl2[k + 1], d);
+                  d = fmaf(row[k + 2], sh[k + 2] + sl2[k + 2], d);
+                  d = fmaf(row[k + 3], sh[k + 3] + sl2[k + 3], d);
+                  dot += (double)d;
+                }
+#pragma unroll
+                for (int k = 0; k < 32; ++k) row[k] *= uc.s;  // dA row a
+                float hi[32], lw[32];
+                split_regs(row, hi, lw);
+                store_row(ops + 2 * kOpBytes, a, hi);  // dA rows (for dK~ = V dA^T)
+                store_row(ops + 3 * kOpBytes, a, lw);
+#pragma unroll
+                for (int n = 0; n < 32; ++n) {  // dA^T rows (for dV = K~ dA)
+                  *reinterpret_cast<float*>(ops + 4 * kOpBytes + elem_off(n, a)) = hi[n];
+                  *reinterpret_cast<float*>(ops + 5 * kOpBytes + elem_off(n, a)) = lw[n];
+                }
+              }
+              // fixed-order dm: 16-lane tree per warp, then warp 0 + warp 1 of the group
+#pragma unroll
+              for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+              if (wq == 1 && lane == 0) *dm_x = dot;
+              fence_proxy_async();
+              tc_fence_before();
+              group_sync(g);
+              if (t == 0) {
+                mbar_arrive(&br->op_ready);
+                if (p.dm_unit) p.dm_unit[u] = uc.coef * (dot + *dm_x);
+              }
+            } else {
+              tc_fence_before();
+            }
+            store_row(X, t, gq);  // staged in the Q tile's slot of the raw stage
+            fence_proxy_async();
+            group_sync(g);
+            if (t == 0) tma_store_4d(&tdq, X, 0, c * kRows, h, b);
+          } else {
+            // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439); dK_i = v_i ? (g - (g.k~)k~)/nk : 0 (:430-437)
+            float dv[32], gk[32];
+            tmem_ld32(D, dv);
+            tmem_ld32(D + 32, gk);
+            tmem_wait_ld();
+            tc_fence_before();
+            const float pr = dot32(gk, xr);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              dv[k] = f ? dv[k] : 0.f;
+              gk[k] = f ? (gk[k] - pr * xr[k]) * inv : 0.f;
+            }
+            if (uc.tn == 0) {  // UsageError in the reference: NaN outputs + status bit
+#pragma unroll
+              for (int k = 0; k < 32; ++k) dv[k] = gk[k] = qnan;
+            }
+            store_row(X, t, gk);
+            store_row(X + kTile, t, dv);
+            fence_proxy_async();
+            group_sync(g);
+            if (t == 0) {
+              tma_store_4d(&tdk, X, 0, c * kRows, h, b);
+              tma_store_4d(&tdv, X + kTile, 0, c * kRows, h, b);
+            }
+          }
+          TC_TRACE(4);
+          ++n_tr;
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
+    }
+    if (t == 0) bulk_wait0();
+  }
+  tc_teardown(tmem, warp);
+}
+
+}  // namespace tc
+
+// ---- host side ----------------------------------------------------------------------
+
+// 4-D map over (D, N, H, B) with a (32, 128, 1, 1) box and 128-byte swizzle
+// (loads zero-fill rows >= N; stores clip them).
+// MN-major reduction operands are loaded with 32-byte granules (the UMMA
+// SWIZZLE_128B_BASE32B layout); K-major operands and stores use 16-byte ones.
+inline bool make_chunk_map(CUtensorMap* map, const void* base, const OpParams& p,
+                           bool granule32 = false) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)p.N, (cuuint64_t)p.H, (cuuint64_t)p.B};
+  cuuint64_t strides[3] = {(cuuint64_t)p.sn * 4, (cuuint64_t)p.sh * 4, (cuuint64_t)p.sb * 4};
+  cuuint32_t box[4] = {32, (cuuint32_t)tc::kRows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             granule32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Sequences of <= 64 rows would leave half of every 128-row chunk empty; the
+// FP32-pipe kernels (kernels_d32.cuh) serve them until units are packed.
+constexpr int64_t kTcMinN = 65;
+
+inline bool tc_layout_ok(const OpParams& p, std::initializer_list<const void*> ptrs) {
+  if (p.D != 32 || p.N < kTcMinN || p.N > tc::kMaxN) return false;
+  if ((p.sn * 4) % 16 || (p.sh * 4) % 16 || (p.sb * 4) % 16) return false;
+  if (p.B * p.H > (1ll << 31) - 1) return false;
+  for (const void* q : ptrs)
+    if (q && (reinterpret_cast<uintptr_t>(q) & 15)) return false;
+  return encode_fn() != nullptr;
+}
+
+template <typename T>
+inline bool tc_fwd_supported(const OpParams& p) {
+  if constexpr (!std::is_same<T, float>::value) {
+    return false;
+  } else {
+    return tc_layout_ok(p, {p.q, p.k, p.v, p.out});
+  }
+}
+template <typename T>
+inline bool tc_bwd_supported(const OpParams& p) {
+  if constexpr (!std::is_same<T, float>::value) {
+    return false;
+  } else {
+    return p.saved_S != nullptr && tc_layout_ok(p, {p.q, p.k, p.v, p.dout, p.dq, p.dk, p.dv});
+  }
+}
+
+// Phase-trace plumbing (trace builds only): a device buffer per launch, dumped
+// to $COTTEN_TRACE_DIR/<fwd|bwd>.bin after the kernel.
+inline void* tc_trace_begin(int grid) {
+#if COTTEN_TC_TRACE
+  static void* buf = nullptr;
+  const size_t bytes = (size_t)grid * 3 * tc::kTraceItems * 8 * sizeof(long long);
+  if (!buf) cudaMalloc(&buf, (size_t)1024 * 3 * tc::kTraceItems * 8 * sizeof(long long));
+  cudaMemset(buf, 0, bytes);
+  return buf;
+#else
+  (void)grid;
+  return nullptr;
+#endif
+}
+inline void tc_trace_end(void* buf, int grid, const char* tag, cudaStream_t st) {
+#if COTTEN_TC_TRACE
+  const char* dir = getenv("COTTEN_TRACE_DIR");
+  if (!dir || !buf) return;
+  const size_t n = (size_t)grid * 3 * tc::kTraceItems * 8;
+  std::vector<long long> h(n);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h.data(), buf, n * sizeof(long long), cudaMemcpyDeviceToHost);
+  std::string path = std::string(dir) + "/" + tag + ".bin";
+  if (FILE* f = fopen(path.c_str(), "wb")) {
+    fwrite(h.data(), sizeof(long long), n, f);
+    fclose(f);
+  }
+#else
+  (void)buf; (void)grid; (void)tag; (void)st;
+#endif
+}
+
+inline int launch_tc_fwd(const OpParams& p, cudaStream_t st) {
+  CUtensorMap mq, mk, mv, mo;
+  if (!make_chunk_map(&mq, p.q, p) || !make_chunk_map(&mk, p.k, p, true) ||
+      !make_chunk_map(&mv, p.v, p, true) || !make_chunk_map(&mo, p.out ? p.out : p.q, p))
+    return -1;
+  const int units = (int)(p.B * p.H);
+  if (cudaFuncSetAttribute(tc::cos_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tc::kSmemBytes) != cudaSuccess)
+    return -1;
+  const int grid = std::min(units, sm_count());
+  OpParams q = p;
+  q.workspace = tc_trace_begin(grid);
+  tc::cos_fwd_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(mq, mk, mv, mo, q);
+  tc_trace_end(q.workspace, grid, "fwd", st);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+inline int launch_tc_bwd(const OpParams& p, cudaStream_t st) {
+  CUtensorMap mq, mk, mv, mg, mdq, mdk, mdv;
+  if (!make_chunk_map(&mq, p.q, p, true) || !make_chunk_map(&mk, p.k, p) ||
+      !make_chunk_map(&mv, p.v, p) || !make_chunk_map(&mg, p.dout, p, true) ||
+      !make_chunk_map(&mdq, p.dq, p) || !make_chunk_map(&mdk, p.dk, p) ||
+      !make_chunk_map(&mdv, p.dv, p))
+    return -1;
+  const int units = (int)(p.B * p.H);
+  if (cudaFuncSetAttribute(tc::cos_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tc::kSmemBytes) != cudaSuccess)
+    return -1;
+  const int grid = std::min(units, sm_count());
+  OpParams q = p;
+  q.workspace = tc_trace_begin(grid);
+  tc::cos_bwd_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(mq, mk, mv, mg, mdq, mdk,
+                                                                     mdv, q);
+  tc_trace_end(q.workspace, grid, "bwd", st);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace cotten

@@ -128,7 +128,11 @@ def assert_parity(res, ref, valid, dtype, m=None, eps=None):
     assert res["dm_total"] == pytest.approx(float(np.sum(res["dm_unit"])), rel=1e-12, abs=1e-12)
 
 
-@pytest.mark.parametrize("flags", [0, _lib.FLAG_FORCE_GENERIC], ids=["fast", "generic"])
+PATHS = [0, _lib.FLAG_FP32_PIPE, _lib.FLAG_FORCE_GENERIC]
+PATH_IDS = ["tcgen05", "fp32pipe", "generic"]
+
+
+@pytest.mark.parametrize("flags", PATHS, ids=PATH_IDS)
 @pytest.mark.parametrize("mask_kind", ["left", "random", "none"])
 def test_ml1m_unit_shape_f32(flags, mask_kind):
     B, H, N, D = 24, 2, 200, 32
@@ -140,12 +144,14 @@ def test_ml1m_unit_shape_f32(flags, mask_kind):
     assert_parity(res, ref, valid, "f32")
 
 
-@pytest.mark.parametrize("N", [1, 2, 31, 32, 33, 50, 127, 200, 257, 513])
-def test_seq_len_edges_f32(N):
+@pytest.mark.parametrize("flags", PATHS[:2], ids=PATH_IDS[:2])
+@pytest.mark.parametrize("N", [1, 2, 7, 8, 9, 31, 32, 33, 50, 127, 128, 129, 200, 255, 256, 257,
+                               513, 1000, 2048])
+def test_seq_len_edges_f32(N, flags):
     B, H, D = 5, 2, 32
     h = inputs.make_host(B, H, N, D, seed=N)
     valid = inputs.left_padded_mask(B, N, N)
-    res = run_gpu(h, valid, 0.75, 1e-6, "f32")
+    res = run_gpu(h, valid, 0.75, 1e-6, "f32", flags)
     assert_parity(res, oracle_for(res["inputs"], valid, 0.75, 1e-6), valid, "f32")
 
 
