@@ -78,8 +78,10 @@ constexpr uint32_t kOffFlags = kOffOps + 6 * 4096;         // 2 x 2 KB bitmasks
 constexpr uint32_t kOffMisc = kOffFlags + 2 * (kMaxN / 8);  // 2 x 16 B unit constants, tmem base
 constexpr uint32_t kOffBar = kOffMisc + 64;
 constexpr uint32_t kSmemBytes = kOffBar + 32 * 8;
-// state operands (32 rows x 128 B each): 0/1 = S-side hi/lo, 2/3 = dA rows hi/lo,
-// 4/5 = dA^T rows hi/lo
+// state operands (32 rows x 128 B each, hi/lo pairs): 0/1 = S rows (bwd: K-major
+// B of dQ~ = dO S^T; fwd: 32-byte granules, MN-major B of O = Q~ S), 2/3 = dA
+// rows (K-major B of dK~ = V dA^T), 4/5 = dA rows in 32-byte granules (MN-major
+// B of dV = K~ dA)
 constexpr uint32_t kOpBytes = 4096;
 
 // TMEM: 512 columns.  Backward: [0, 64) G; group g's buffer at kBwdBuf0 + 192 g:
@@ -229,20 +231,40 @@ __device__ __forceinline__ void store_row(uint8_t* tile, int row, const float (&
 __device__ __forceinline__ uint32_t chunk_off32(int row, int j) {
   return (uint32_t)row * 128u + ((uint32_t)((j >> 1) ^ (row & 3)) << 5) + ((uint32_t)(j & 1) << 4);
 }
+// Rows r, r+1, .. of a warp hit only 4 distinct 16-byte bank groups if every
+// lane walks its granules in the same order; lanes with bit 2 of the row set
+// take the two halves of each 32-byte granule in swapped order, so each
+// LDS/STS.128 of the warp spans all 8 bank groups (4 wavefronts, the minimum).
 __device__ __forceinline__ void load_row32(const uint8_t* tile, int row, float (&x)[32]) {
+  const uint32_t sw = (uint32_t)((row >> 2) & 1) << 4;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float4 v = *reinterpret_cast<const float4*>(tile + chunk_off32(row, j));
-    x[4 * j] = v.x;
-    x[4 * j + 1] = v.y;
-    x[4 * j + 2] = v.z;
-    x[4 * j + 3] = v.w;
+  for (int q = 0; q < 4; ++q) {
+    const uint8_t* g = tile + (uint32_t)row * 128u + ((uint32_t)(q ^ (row & 3)) << 5);
+    const float4 a = *reinterpret_cast<const float4*>(g + sw);
+    const float4 b = *reinterpret_cast<const float4*>(g + (sw ^ 16u));
+    const bool s = sw != 0;
+    x[8 * q + 0] = s ? b.x : a.x;
+    x[8 * q + 1] = s ? b.y : a.y;
+    x[8 * q + 2] = s ? b.z : a.z;
+    x[8 * q + 3] = s ? b.w : a.w;
+    x[8 * q + 4] = s ? a.x : b.x;
+    x[8 * q + 5] = s ? a.y : b.y;
+    x[8 * q + 6] = s ? a.z : b.z;
+    x[8 * q + 7] = s ? a.w : b.w;
   }
 }
-// Round to the nearest tf32 (ties away from zero): exact in tf32, so the
-// tensor core reads it unchanged.  Operands are split x = hi + lo with
-// hi = tf32(x), |x - hi| <= 2^-11 |x|, and lo = tf32(x - hi), so what the
-// MMAs see differs from x by at most 2^-22 |x|.
+__device__ __forceinline__ void store_row32(uint8_t* tile, int row, const float (&x)[32]) {
+  const uint32_t sw = (uint32_t)((row >> 2) & 1) << 4;
+  const bool s = sw != 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint8_t* g = tile + (uint32_t)row * 128u + ((uint32_t)(q ^ (row & 3)) << 5);
+    const float4 lo4 = make_float4(x[8 * q], x[8 * q + 1], x[8 * q + 2], x[8 * q + 3]);
+    const float4 hi4 = make_float4(x[8 * q + 4], x[8 * q + 5], x[8 * q + 6], x[8 * q + 7]);
+    *reinterpret_cast<float4*>(g + sw) = s ? hi4 : lo4;
+    *reinterpret_cast<float4*>(g + (sw ^ 16u)) = s ? lo4 : hi4;
+  }
+}
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
@@ -273,39 +295,112 @@ __device__ __forceinline__ void store_split(uint8_t* hi_tile, uint8_t* lo_tile, 
 }
 __device__ __forceinline__ void store_split32(uint8_t* hi_tile, uint8_t* lo_tile, int row,
                                               const float (&x)[32]) {
+  float h[32], l[32];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float h[4], l[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      h[e] = tf32_hi(x[4 * j + e]);
-      l[e] = tf32_lo(x[4 * j + e], h[e]);
-    }
-    *reinterpret_cast<float4*>(hi_tile + chunk_off32(row, j)) = make_float4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<float4*>(lo_tile + chunk_off32(row, j)) = make_float4(l[0], l[1], l[2], l[3]);
+  for (int k = 0; k < 32; ++k) {
+    h[k] = tf32_hi(x[k]);
+    l[k] = tf32_lo(x[k], h[k]);
   }
+  store_row32(hi_tile, row, h);
+  store_row32(lo_tile, row, l);
 }
+// ---- packed fp32x2 row arithmetic (FFMA2 / FMUL2: half the FP instructions) ----
+__device__ __forceinline__ float2 f2p(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float sumsq(const float (&x)[32]) {
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  float2 a0 = f2p(0.f, 0.f), a1 = f2p(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < 32; k += 4) {
-    a0 = fmaf(x[k], x[k], a0);
-    a1 = fmaf(x[k + 1], x[k + 1], a1);
-    a2 = fmaf(x[k + 2], x[k + 2], a2);
-    a3 = fmaf(x[k + 3], x[k + 3], a3);
+    a0 = __ffma2_rn(f2p(x[k], x[k + 1]), f2p(x[k], x[k + 1]), a0);
+    a1 = __ffma2_rn(f2p(x[k + 2], x[k + 3]), f2p(x[k + 2], x[k + 3]), a1);
   }
-  return (a0 + a1) + (a2 + a3);
+  return (a0.x + a1.x) + (a0.y + a1.y);
 }
 __device__ __forceinline__ float dot32(const float (&x)[32], const float (&y)[32]) {
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  float2 a0 = f2p(0.f, 0.f), a1 = f2p(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < 32; k += 4) {
-    a0 = fmaf(x[k], y[k], a0);
-    a1 = fmaf(x[k + 1], y[k + 1], a1);
-    a2 = fmaf(x[k + 2], y[k + 2], a2);
-    a3 = fmaf(x[k + 3], y[k + 3], a3);
+    a0 = __ffma2_rn(f2p(x[k], x[k + 1]), f2p(y[k], y[k + 1]), a0);
+    a1 = __ffma2_rn(f2p(x[k + 2], x[k + 3]), f2p(y[k + 2], y[k + 3]), a1);
   }
-  return (a0 + a1) + (a2 + a3);
+  return (a0.x + a1.x) + (a0.y + a1.y);
+}
+__device__ __forceinline__ void scale32(float (&x)[32], float s) {
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const float2 v = __fmul2_rn(f2p(x[k], x[k + 1]), f2p(s, s));
+    x[k] = v.x;
+    x[k + 1] = v.y;
+  }
+}
+// g <- (g - pr x) * inv   (the cosine-normalisation Jacobian, attention.cpp:421-437)
+__device__ __forceinline__ void jacobian32(float (&g)[32], const float (&x)[32], float pr,
+                                           float inv) {
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const float2 v =
+        __fmul2_rn(__ffma2_rn(f2p(x[k], x[k + 1]), f2p(-pr, -pr), f2p(g[k], g[k + 1])), f2p(inv, inv));
+    g[k] = v.x;
+    g[k + 1] = v.y;
+  }
+}
+// Zero a row unless f (bit mask, NaN-safe: padded rows are never multiplied).
+__device__ __forceinline__ void keep_if(float (&x)[32], bool f) {
+  const uint32_t m = f ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) x[k] = __uint_as_float(__float_as_uint(x[k]) & m);
+}
+// 3xTF32 split of a row: h = x with the low 13 mantissa bits cleared (exact
+// in tf32), l = x - h (exact in fp32; |l| < 2^-10 |x|, the tensor core's own
+// truncation of l costs < 2^-20 |x|).  Optionally NaN-safe masked to zero.
+__device__ __forceinline__ void split32(const float (&x)[32], float (&h)[32], float (&l)[32],
+                                        uint32_t mask = 0xFFFFFFFFu) {
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const float h0 = __uint_as_float(__float_as_uint(x[k]) & (0xFFFFE000u & mask));
+    const float h1 = __uint_as_float(__float_as_uint(x[k + 1]) & (0xFFFFE000u & mask));
+    const float2 lv = __ffma2_rn(f2p(h0, h1), f2p(-1.f, -1.f), f2p(x[k], x[k + 1]));
+    h[k] = h0;
+    h[k + 1] = h1;
+    l[k] = __uint_as_float(__float_as_uint(lv.x) & mask);
+    l[k + 1] = __uint_as_float(__float_as_uint(lv.y) & mask);
+  }
+}
+// Rows of a 32-byte-granule tile in "lane order": x[8q..8q+3] is the half of
+// granule q the lane touches first (see load_row32), x[8q+4..8q+7] the other.
+// Element-wise work (norms, scaling, hi/lo split) does not care about the order,
+// so tiles that are only re-stored in the same layout skip the unswizzle selects.
+__device__ __forceinline__ void load_row32_raw(const uint8_t* tile, int row, float (&x)[32]) {
+  const uint32_t sw = (uint32_t)((row >> 2) & 1) << 4;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint8_t* g = tile + (uint32_t)row * 128u + ((uint32_t)(q ^ (row & 3)) << 5);
+    const float4 a = *reinterpret_cast<const float4*>(g + sw);
+    const float4 b = *reinterpret_cast<const float4*>(g + (sw ^ 16u));
+    x[8 * q + 0] = a.x; x[8 * q + 1] = a.y; x[8 * q + 2] = a.z; x[8 * q + 3] = a.w;
+    x[8 * q + 4] = b.x; x[8 * q + 5] = b.y; x[8 * q + 6] = b.z; x[8 * q + 7] = b.w;
+  }
+}
+__device__ __forceinline__ void store_row32_raw(uint8_t* tile, int row, const float (&x)[32]) {
+  const uint32_t sw = (uint32_t)((row >> 2) & 1) << 4;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint8_t* g = tile + (uint32_t)row * 128u + ((uint32_t)(q ^ (row & 3)) << 5);
+    *reinterpret_cast<float4*>(g + sw) = make_float4(x[8 * q], x[8 * q + 1], x[8 * q + 2], x[8 * q + 3]);
+    *reinterpret_cast<float4*>(g + (sw ^ 16u)) =
+        make_float4(x[8 * q + 4], x[8 * q + 5], x[8 * q + 6], x[8 * q + 7]);
+  }
+}
+// lane order -> natural column order (and back: the map is an involution)
+__device__ __forceinline__ void unswap32(float (&x)[32], int row) {
+  const bool s = (row >> 2) & 1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float a = x[8 * q + e], b = x[8 * q + 4 + e];
+      x[8 * q + e] = s ? b : a;
+      x[8 * q + 4 + e] = s ? a : b;
+    }
 }
 // Element (n, k) of a 32-row operand buffer (row n, column k).
 __device__ __forceinline__ uint32_t elem_off(int n, int k) {
@@ -317,6 +412,16 @@ __device__ __forceinline__ bool flag_at(const uint32_t* fl, int r) {
 }
 
 // ---- the mask warp ------------------------------------------------------------
+
+// s = exp(-m ln n) and coef = -ln(n) s in fp64 (attention.cpp:304, :403, :408);
+// out of line: one call per unit, keeps the fp64 libm expansion out of the
+// instruction-cache working set of the hot loops.
+__device__ __noinline__ void unit_scale(double m, int n, float* s_out, double* coef_out) {
+  const double ln = log((double)n);
+  const float s = (float)exp(-m * ln);
+  *s_out = s;
+  *coef_out = -ln * (double)s;
+}
 
 // Bitmask of valid rows + true_n + the fp64 scale constants of unit (b).
 __device__ __forceinline__ void mask_unit(const OpParams& p, int64_t b, uint32_t* fl,
@@ -345,10 +450,7 @@ __device__ __forceinline__ void mask_unit(const OpParams& p, int64_t b, uint32_t
     UnitConst c;
     c.tn = cnt;
     if (cnt > 0) {
-      const double ln = log((double)cnt);
-      const double s = exp(-p.m * ln);  // attention.cpp:304 / :403, fp64
-      c.s = (float)s;
-      c.coef = -ln * (double)c.s;  // attention.cpp:408
+      unit_scale(p.m, cnt, &c.s, &c.coef);
     } else {  // UsageError in the reference (attention.cpp:44): NaN outputs + status bit
       c.s = __int_as_float(0x7fc00000);
       c.coef = __longlong_as_double(0x7ff8000000000000ll);
@@ -377,14 +479,18 @@ __device__ __forceinline__ void issue_reduction(uint32_t d, uint32_t xh, uint32_
 // M=128, N=32, K=8.  A from TMEM keeps these small-N MMAs off the shared-
 // memory port (an SS MMA would re-read its 4 KB A tile for every 16-cycle
 // instruction).
+template <bool kBMN>
 __device__ __forceinline__ void issue_rowout_ts(uint32_t d, uint32_t ah, uint32_t bh, uint32_t bl) {
-  const uint32_t id = idesc_tf32(128, 32, false, false);
+  // B K-major (row n holds B[.][n], 16-byte granules): k-step = 32 bytes along the row;
+  // B MN-major (row k holds B[k][.], 32-byte granules): k-step = 8 rows = 1 KB.
+  const uint32_t id = idesc_tf32(128, 32, false, kBMN);
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
-    const uint32_t o = 32u * kk;
-    mma_tf32_ts(d, ah + 8 * kk, sdesc(bh + o, 16u, 1024u), id, kk > 0 ? 1u : 0u);
-    mma_tf32_ts(d, ah + 8 * kk, sdesc(bl + o, 16u, 1024u), id, 1u);
-    mma_tf32_ts(d, ah + 32 + 8 * kk, sdesc(bh + o, 16u, 1024u), id, 1u);
+    const uint64_t dh = kBMN ? sdesc(bh + 1024u * kk, 4096u, 512u, 1u) : sdesc(bh + 32u * kk, 16u, 1024u);
+    const uint64_t dl = kBMN ? sdesc(bl + 1024u * kk, 4096u, 512u, 1u) : sdesc(bl + 32u * kk, 16u, 1024u);
+    mma_tf32_ts(d, ah + 8 * kk, dh, id, kk > 0 ? 1u : 0u);
+    mma_tf32_ts(d, ah + 8 * kk, dl, id, 1u);
+    mma_tf32_ts(d, ah + 32 + 8 * kk, dh, id, 1u);
   }
 }
 __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&r)[32]) {
@@ -393,13 +499,10 @@ __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&r)[32]) {
 }
 // Split a row into hi / lo and store both as TMEM A-operand columns of this
 // thread's lane: hi at [col, col+32), lo at [col+32, col+64).
-__device__ __forceinline__ void tmem_store_split(uint32_t taddr, const float (&x)[32]) {
+__device__ __forceinline__ void tmem_store_split(uint32_t taddr, const float (&x)[32],
+                                                 uint32_t mask = 0xFFFFFFFFu) {
   float h[32], l[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    h[k] = tf32_hi(x[k]);
-    l[k] = tf32_lo(x[k], h[k]);
-  }
+  split32(x, h, l, mask);
   tmem_st32(taddr, h);
   tmem_st32(taddr + 32, l);
 }
@@ -534,12 +637,6 @@ __device__ __forceinline__ void split_regs(const float (&x)[32], float (&h)[32],
     l[k] = tf32_lo(x[k], h[k]);
   }
 }
-__device__ __forceinline__ void store_row32(uint8_t* tile, int row, const float (&x)[32]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    *reinterpret_cast<float4*>(tile + chunk_off32(row, j)) =
-        make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
-}
 
 // Release the raw stage of this group's previous item once its TMA store (if
 // any) has finished reading it.
@@ -616,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
               issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c == 0);
             } else {  // O = Q~ S (attention.cpp:379-387); B row n = S column n
               const uint32_t D = tmem + kFwdBuf0 + kFwdBufCols * g;
-              issue_rowout_ts(D, D + 32, base + kOffOps, base + kOffOps + kOpBytes);
+              issue_rowout_ts<true>(D, D + 32, base + kOffOps, base + kOffOps + kOpBytes);
             }
             TC_TRACE_MMA(2);
             mma_commit(&br->mma_done[g]);
@@ -653,25 +750,27 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
           mbar_wait(&br->raw_full[st], (it >> 2) & 1);
           TC_TRACE(1);
           if (ps == 0) {  // K~ (masked, attention.cpp:334-343) and V, 32-byte-granule tiles
-            float kx[32], vx[32];
-            load_row32(X, t, kx);
-            load_row32(X + kTile, t, vx);
+            float kx[32], vx[32], h[32], l[32];
+            load_row32_raw(X, t, kx);  // lane order: only re-stored in the same layout
+            load_row32_raw(X + kTile, t, vx);
             const bool f = r < N && flag_at(fl, r);
             const float ss = sumsq(kx) + eps;
             const float iv = rsqrtf(ss);
-#pragma unroll
-            for (int k = 0; k < 32; ++k) kx[k] = f ? kx[k] * iv : 0.f;  // selected: NaN-safe
+            scale32(kx, iv);
             if (norms && r < N) norms[N + r] = f ? ss * iv : 1.0f;  // :336, :343
             release_prev(br, prev_st, t);
-            store_split32(X, Y, t, kx);
-            store_split32(X + kTile, Y + kTile, t, vx);
-          } else {  // Q~ for every row (attention.cpp:366-377)
+            split32(kx, h, l, f ? 0xFFFFFFFFu : 0u);  // padded rows: exact zeros, NaN-safe
+            store_row32_raw(X, t, h);
+            store_row32_raw(Y, t, l);
+            split32(vx, h, l);
+            store_row32_raw(X + kTile, t, h);
+            store_row32_raw(Y + kTile, t, l);
+          } else {  // Q~ for every row (attention.cpp:366-377), TMEM A operand of O = Q~ S
             float qx[32];
             load_row(X, t, qx);
             const float ss = sumsq(qx) + eps;
             const float iv = rsqrtf(ss);
-#pragma unroll
-            for (int k = 0; k < 32; ++k) qx[k] *= iv;
+            scale32(qx, iv);
             if (norms && r < N) norms[r] = ss * iv;
             release_prev(br, prev_st, t);
             tmem_store_split(tmem + kFwdBuf0 + kFwdBufCols * g + 32 + lane_base, qx);
@@ -700,12 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
                   for (int q = 0; q < 8; ++q)
                     gs[q] = make_float4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
                 }
-#pragma unroll
-                for (int n = 0; n < 32; ++n) {
-                  const float hv = tf32_hi(row[n]);
-                  *reinterpret_cast<float*>(ops + elem_off(n, a)) = hv;
-                  *reinterpret_cast<float*>(ops + kOpBytes + elem_off(n, a)) = tf32_lo(row[n], hv);
-                }
+                store_split32(ops, ops + kOpBytes, a, row);  // S rows: MN-major B of O = Q~ S
               }
               fence_proxy_async();
               tc_fence_before();
@@ -716,8 +810,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
             float acc[32];
             tmem_ld_row(tmem + kFwdBuf0 + kFwdBufCols * g + lane_base, acc);
             tc_fence_before();
-#pragma unroll
-            for (int k = 0; k < 32; ++k) acc[k] *= uc.s;
+            scale32(acc, uc.s);
             store_row(X, t, acc);
             fence_proxy_async();
             group_sync(g);
@@ -795,12 +888,12 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               const int rows = min(kRows, N - c * kRows);
               issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c == 0);
               // dQ~ (unscaled) = dO S^T (:410-411): A = dO hi/lo in TMEM, B row n = S row n
-              issue_rowout_ts(D, D + 64, opS, opS + kOpBytes);
+              issue_rowout_ts<false>(D, D + 64, opS, opS + kOpBytes);
             } else {
-              // dV = K~ dA (:416): B row n = dA column n
-              issue_rowout_ts(D, D + 64, opAt, opAt + kOpBytes);
-              // dK~ = V dA^T (:415): B row n = dA row n
-              issue_rowout_ts(D + 32, D + 128, opA, opA + kOpBytes);
+              // dV = K~ dA (:416): B = dA row-major as an MN-major operand
+              issue_rowout_ts<true>(D, D + 64, opAt, opAt + kOpBytes);
+              // dK~ = V dA^T (:415): B row n = dA row n (K-major)
+              issue_rowout_ts<false>(D + 32, D + 128, opA, opA + kOpBytes);
             }
             TC_TRACE_MMA(2);
             mma_commit(&br->mma_done[g]);
@@ -851,21 +944,23 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
           if (ps == 0) {
             // Q~ every row (:366-377, used again in :421-428); rows past N are exact
             // zeros in G even for eps = 0.  Tiles use the 32-byte-granule swizzle.
-            float gy[32];
-            load_row32(X, t, xr);
-            load_row32(X + kTile, t, gy);
+            float gy[32], h[32], l[32];
+            load_row32_raw(X, t, xr);
+            load_row32_raw(X + kTile, t, gy);
             inv = rsqrtf(sumsq(xr) + eps);
-            const bool in = r < N;
-#pragma unroll
-            for (int k = 0; k < 32; ++k) xr[k] = in ? xr[k] * inv : 0.f;
+            scale32(xr, r < N ? inv : 0.f);
             release_prev(br, prev_st, t);
-            store_split32(X, Y, t, xr);
-            float hv[32], lv[32];
-            split_regs(gy, hv, lv);
-            store_row32(X + kTile, t, hv);
-            store_row32(Y + kTile, t, lv);
-            tmem_st32(D + 64, hv);  // dO as the TMEM A operand of dQ~ = dO S^T
-            tmem_st32(D + 96, lv);
+            split32(xr, h, l);
+            store_row32_raw(X, t, h);
+            store_row32_raw(Y, t, l);
+            unswap32(xr, t);  // natural order: the dQ Jacobian pairs it with TMEM columns
+            split32(gy, h, l);
+            store_row32_raw(X + kTile, t, h);
+            store_row32_raw(Y + kTile, t, l);
+            unswap32(h, t);  // dO as the TMEM A operand of dQ~ = dO S^T
+            unswap32(l, t);
+            tmem_st32(D + 64, h);
+            tmem_st32(D + 96, l);
             if (c == 0) {  // S rows (row n = S row n) for dQ~ = dO S^T
 #pragma unroll
               for (int e2 = 0; e2 < 2; ++e2) {
@@ -882,17 +977,16 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             }
             tmem_wait_st();
             tc_fence_before();
-          } else {  // K~ masked (:334-343), V as is
+          } else {  // K~ masked (:334-343) and V: TMEM A operands of dV = K~ dA, dK~ = V dA^T
             float vy[32];
             load_row(X, t, xr);
             load_row(X + kTile, t, vy);
             f = r < N && flag_at(fl, r);
             inv = rsqrtf(sumsq(xr) + eps);
-#pragma unroll
-            for (int k = 0; k < 32; ++k) xr[k] = f ? xr[k] * inv : 0.f;  // selected: NaN-safe
+            scale32(xr, inv);  // padded rows may hold anything: masked below, never multiplied in
             release_prev(br, prev_st, t);
-            tmem_store_split(D + 64, xr);   // K~: A of dV = K~ dA
-            tmem_store_split(D + 128, vy);  // V:  A of dK~ = V dA^T
+            tmem_store_split(D + 64, xr, f ? 0xFFFFFFFFu : 0u);
+            tmem_store_split(D + 128, vy);
             tmem_wait_st();
             tc_fence_before();
           }
@@ -910,11 +1004,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428)
             float gq[32];
             tmem_ld_row(D, gq);
-#pragma unroll
-            for (int k = 0; k < 32; ++k) gq[k] *= uc.s;
-            const float pr = dot32(gq, xr);
-#pragma unroll
-            for (int k = 0; k < 32; ++k) gq[k] = (gq[k] - pr * xr[k]) * inv;
+            scale32(gq, uc.s);
+            jacobian32(gq, xr, dot32(gq, xr), inv);
             if (c == C - 1) {
               // G complete: dm (:408), dA = s G (:412-413) as both state operands
               float row[32];
@@ -937,13 +1028,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
                 for (int k = 0; k < 32; ++k) row[k] *= uc.s;  // dA row a
                 float hi[32], lw[32];
                 split_regs(row, hi, lw);
-                store_row(ops + 2 * kOpBytes, a, hi);  // dA rows (for dK~ = V dA^T)
+                store_row(ops + 2 * kOpBytes, a, hi);  // dA rows, K-major B of dK~ = V dA^T
                 store_row(ops + 3 * kOpBytes, a, lw);
-#pragma unroll
-                for (int n = 0; n < 32; ++n) {  // dA^T rows (for dV = K~ dA)
-                  *reinterpret_cast<float*>(ops + 4 * kOpBytes + elem_off(n, a)) = hi[n];
-                  *reinterpret_cast<float*>(ops + 5 * kOpBytes + elem_off(n, a)) = lw[n];
-                }
+                store_row32(ops + 4 * kOpBytes, a, hi);  // dA rows, MN-major B of dV = K~ dA
+                store_row32(ops + 5 * kOpBytes, a, lw);
               }
               // fixed-order dm: 16-lane tree per warp, then warp 0 + warp 1 of the group
 #pragma unroll
@@ -970,12 +1058,9 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             tmem_ld32(D + 32, gk);
             tmem_wait_ld();
             tc_fence_before();
-            const float pr = dot32(gk, xr);
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              dv[k] = f ? dv[k] : 0.f;
-              gk[k] = f ? (gk[k] - pr * xr[k]) * inv : 0.f;
-            }
+            jacobian32(gk, xr, dot32(gk, xr), inv);
+            keep_if(dv, f);  // padded rows: exact zeros (:437, :439)
+            keep_if(gk, f);
             if (uc.tn == 0) {  // UsageError in the reference: NaN outputs + status bit
 #pragma unroll
               for (int k = 0; k < 32; ++k) dv[k] = gk[k] = qnan;
