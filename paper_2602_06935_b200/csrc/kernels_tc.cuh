@@ -23,7 +23,7 @@
 //     products), A = the chunk (K-major SW128), B = the 32x32 state operand
 //     (S, S^T, dA or dA^T, split hi/lo) written by the workers.
 //
-// Warp roles (352 threads, one CTA per SM, persistent over units):
+// Warp roles (384 threads, one CTA per SM, persistent over units):
 //   warps 0-7  two worker groups of 4 warps; group g takes chunks i = g (mod 2)
 //              and thread t owns row t of its chunk (= TMEM lane t): row norms,
 //              masking, hi/lo split (hi in place in the TMA stage, lo into the
@@ -36,6 +36,8 @@
 //   warp 10    mask warp: up to two units ahead, valid bytes -> bitmask,
 //              true_n, s = exp(-m ln n), coef = -ln(n) s in fp64
 //              (attention.cpp:303-304, :402-408).
+//   warp 11    store warp: TMA-stores each chunk's staged outputs and hands
+//              the stage back to the producer once the store has read it.
 // Nothing but the outputs, S (4 KB per unit) and dm reach HBM.
 #pragma once
 #include <cuda.h>
@@ -68,7 +70,9 @@ constexpr int kWorkerWarps = 4 * kGroups;
 constexpr int kWarpProducer = kWorkerWarps;
 constexpr int kWarpMma = kWorkerWarps + 1;
 constexpr int kWarpMask = kWorkerWarps + 2;
-constexpr int kThreads = (kWorkerWarps + 3) * 32;
+constexpr int kWarpStore = kWorkerWarps + 3;
+// 12 warps: registers are allocated as if for 12 warps anyway (168 per thread).
+constexpr int kThreads = (kWorkerWarps + 4) * 32;
 
 // Shared-memory plan (bytes; every operand region 1024-aligned for SW128).
 constexpr uint32_t kOffRaw = 0;
@@ -76,7 +80,7 @@ constexpr uint32_t kOffLo = kOffRaw + kRaw * kStage;       // 2 lo buffers
 constexpr uint32_t kOffOps = kOffLo + 2 * kStage;          // 6 x 4 KB state operands
 constexpr uint32_t kOffFlags = kOffOps + 6 * 4096;         // 2 x 2 KB bitmasks
 constexpr uint32_t kOffMisc = kOffFlags + 2 * (kMaxN / 8);  // 2 x 16 B unit constants, tmem base
-constexpr uint32_t kOffBar = kOffMisc + 64;
+constexpr uint32_t kOffBar = kOffMisc + 128;  // misc: UnitConst[2], tmem base, dm partials[4]
 constexpr uint32_t kSmemBytes = kOffBar + 32 * 8;
 // state operands (32 rows x 128 B each, hi/lo pairs): 0/1 = S rows (bwd: K-major
 // B of dQ~ = dO S^T; fwd: 32-byte granules, MN-major B of O = Q~ S), 2/3 = dA
@@ -546,6 +550,10 @@ struct Bars {
   uint64_t split_full[2], mma_done[2];  // workers <-> MMA issuer (group = item & 1)
   uint64_t op_ready;                    // state operand (S or dA) written, per unit
   uint64_t fl_full[2], fl_empty[2];     // mask warp <-> workers (slot = unit & 1)
+  // workers -> store warp: chunk outputs staged (or none) and the stage's MMAs done.
+  // Indexed by stage, not group: a stage is reloaded only after the store warp
+  // released it, so a group can never complete two phases ahead of the waiter.
+  uint64_t staged[4];
 };
 static_assert(sizeof(Bars) <= 256, "barrier area");
 
@@ -567,6 +575,7 @@ __device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* 
       mbar_init(&br->fl_full[i], 1);
       mbar_init(&br->fl_empty[i], kWorkerWarps);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&br->staged[i], 4);
     mbar_init(&br->op_ready, 1);
     d32::fence_barrier_init();
   }
@@ -605,28 +614,51 @@ __device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars
 }
 
 // ---- reduction epilogue (S or G) --------------------------------------------------
-// D (M=64 layout: row m at lane (m%16) + 32(m/16)) -> full 32x32 row a = 16 wq + l
-// in the group's warps wq < 2, lanes < 16.  scratch: 4 KB of free smem.
-__device__ __forceinline__ bool reduce_rows(uint32_t tmem, uint8_t* scratch, int wq, int lane,
-                                            int g, float (&row)[32]) {
+// The M=64 accumulator (row m at lane (m%16) + 32(m/16); rows 0-31 x_hi, 32-63
+// x_lo; columns 0-31 y_hi, 32-63 y_lo) is folded into R = sum of the four
+// products, spread over the whole group: thread t gets row a = t/4, columns
+// [8(t%4), 8(t%4)+8).  scratch: 8 KB of free smem (two 32-row partial tiles).
+__device__ __forceinline__ void reduce_rows8(uint32_t tmem, uint8_t* scratch, int wq, int lane,
+                                             int g, int t, float (&r8)[8]) {
   float a[32], c[32];
   const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16);
   tmem_ld32(ta, a);
   tmem_ld32(ta + 32, c);
   tmem_wait_ld();
+  if (lane < 16) {
 #pragma unroll
-  for (int k = 0; k < 32; ++k) row[k] = a[k] + c[k];  // x.. y_hi + x.. y_lo
-  const int ra = 16 * (wq & 1) + lane;               // row a held by this lane
-  if (wq >= 2 && lane < 16) store_row(scratch, ra, row);
-  group_sync(g);
-  const bool own = wq < 2 && lane < 16;
-  if (own) {
-    float o[32];
-    load_row(scratch, ra, o);
-#pragma unroll
-    for (int k = 0; k < 32; ++k) row[k] += o[k];  // + x_lo y
+    for (int k = 0; k < 32; ++k) a[k] += c[k];  // x.. y_hi + x.. y_lo
+    store_row(scratch + (wq >> 1) * 4096, 16 * (wq & 1) + lane, a);
   }
-  return own;
+  group_sync(g);
+  const int ra = t >> 2, q = t & 3;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float4 u = *reinterpret_cast<const float4*>(scratch + chunk_off(ra, 2 * q + h));
+    const float4 v = *reinterpret_cast<const float4*>(scratch + 4096 + chunk_off(ra, 2 * q + h));
+    r8[4 * h + 0] = u.x + v.x;
+    r8[4 * h + 1] = u.y + v.y;
+    r8[4 * h + 2] = u.z + v.z;
+    r8[4 * h + 3] = u.w + v.w;
+  }
+}
+// 8 columns [8q, 8q+8) of row a as hi / lo into a K-major (16-byte granule)
+// and / or an MN-major (32-byte granule) state operand.
+__device__ __forceinline__ void split8(const float (&x)[8], float (&h)[8], float (&l)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    h[k] = tf32_hi(x[k]);
+    l[k] = tf32_lo(x[k], h[k]);
+  }
+}
+__device__ __forceinline__ void store8_k(uint8_t* op, int a, int q, const float (&x)[8]) {
+  *reinterpret_cast<float4*>(op + chunk_off(a, 2 * q)) = make_float4(x[0], x[1], x[2], x[3]);
+  *reinterpret_cast<float4*>(op + chunk_off(a, 2 * q + 1)) = make_float4(x[4], x[5], x[6], x[7]);
+}
+__device__ __forceinline__ void store8_mn(uint8_t* op, int a, int q, const float (&x)[8]) {
+  uint8_t* gp = op + (uint32_t)a * 128u + ((uint32_t)(q ^ (a & 3)) << 5);
+  *reinterpret_cast<float4*>(gp) = make_float4(x[0], x[1], x[2], x[3]);
+  *reinterpret_cast<float4*>(gp + 16) = make_float4(x[4], x[5], x[6], x[7]);
 }
 
 // hi / lo split of a row into two register arrays.
@@ -638,13 +670,13 @@ __device__ __forceinline__ void split_regs(const float (&x)[32], float (&h)[32],
   }
 }
 
-// Release the raw stage of this group's previous item once its TMA store (if
-// any) has finished reading it.
-__device__ __forceinline__ void release_prev(Bars* br, int& prev_st, int t) {
-  if (prev_st >= 0 && t == 0) {
-    bulk_wait_read0();
-    mbar_arrive(&br->raw_empty[prev_st]);
-  }
+// Arrive on the group's "staged" barrier (one arrival per warp): the chunk's
+// outputs are in its raw stage (or it has none) and the MMAs that read the
+// stage are complete, so the store warp may store it and recycle the stage.
+__device__ __forceinline__ void arrive_staged(Bars* br, int st, int lane) {
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&br->staged[st]);
 }
 
 // ======================================================================================
@@ -723,6 +755,24 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
     }
   } else if (warp == kWarpMask) {
     mask_loop(p, smem, br, lane);
+  } else if (warp == kWarpStore) {  // ===== TMA stores of staged outputs; stage recycling =====
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int ps = 0; ps < P; ++ps)
+          for (int c = 0; c < C; ++c, ++it) {
+            const int st = it & 3, g = it & 1;
+            mbar_wait(&br->staged[st], (it >> 2) & 1);
+            if (ps == 1 && p.out) {
+              tma_store_4d(&to, smem + kOffRaw + st * kStage, 0, c * kRows, h, b);
+              bulk_wait_read0();
+            }
+            mbar_arrive(&br->raw_empty[st]);
+          }
+      }
+      bulk_wait0();
+    }
   } else {  // ===== workers: group g takes items it = g (mod 2); thread t owns chunk row t =====
     const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
     const float eps = (float)p.eps;
@@ -730,7 +780,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
     float* norms_all = static_cast<float*>(p.saved_norms);
     float* gS_all = static_cast<float*>(p.saved_S);
     const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
-    int it = 0, j = 0, prev_st = -1, n_tr = 0;
+    int it = 0, j = 0, n_tr = 0;
     (void)n_tr;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int b = u / H, h = u - b * H;
@@ -758,7 +808,6 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
             const float iv = rsqrtf(ss);
             scale32(kx, iv);
             if (norms && r < N) norms[N + r] = f ? ss * iv : 1.0f;  // :336, :343
-            release_prev(br, prev_st, t);
             split32(kx, h, l, f ? 0xFFFFFFFFu : 0u);  // padded rows: exact zeros, NaN-safe
             store_row32_raw(X, t, h);
             store_row32_raw(Y, t, l);
@@ -772,12 +821,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
             const float iv = rsqrtf(ss);
             scale32(qx, iv);
             if (norms && r < N) norms[r] = ss * iv;
-            release_prev(br, prev_st, t);
             tmem_store_split(tmem + kFwdBuf0 + kFwdBufCols * g + 32 + lane_base, qx);
             tmem_wait_st();
             tc_fence_before();
           }
-          prev_st = st;
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&br->split_full[g]);
@@ -788,19 +835,19 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
           tc_fence_after();
           TC_TRACE(3);
           if (ps == 0) {
-            if (c == C - 1) {  // S complete: saved S + the O operand (row n = S column n)
-              float row[32];
-              const bool own = reduce_rows(tmem, Y + kTile, wq, lane, g, row);
-              if (own) {
-                const int a = 16 * wq + lane;
-                if (gS_all) {
-                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024 + a * 32);
-#pragma unroll
-                  for (int q = 0; q < 8; ++q)
-                    gs[q] = make_float4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
-                }
-                store_split32(ops, ops + kOpBytes, a, row);  // S rows: MN-major B of O = Q~ S
+            arrive_staged(br, st, lane);  // no outputs: the stage is free once the MMAs are done
+            if (c == C - 1) {  // S complete: saved S + the MN-major B operand of O = Q~ S
+              float s8[8], h8[8], l8[8];
+              reduce_rows8(tmem, Y + kTile, wq, lane, g, t, s8);
+              const int a = t >> 2, q = t & 3;
+              if (gS_all) {  // coalesced: a warp writes 8 whole rows of S
+                float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024 + a * 32 + 8 * q);
+                gs[0] = make_float4(s8[0], s8[1], s8[2], s8[3]);
+                gs[1] = make_float4(s8[4], s8[5], s8[6], s8[7]);
               }
+              split8(s8, h8, l8);
+              store8_mn(ops, a, q, h8);
+              store8_mn(ops + kOpBytes, a, q, l8);
               fence_proxy_async();
               tc_fence_before();
               group_sync(g);
@@ -812,9 +859,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
             tc_fence_before();
             scale32(acc, uc.s);
             store_row(X, t, acc);
-            fence_proxy_async();
-            group_sync(g);
-            if (t == 0 && O) tma_store_4d(&to, X, 0, c * kRows, h, b);
+            TC_TRACE(5);
+            arrive_staged(br, st, lane);
           }
           TC_TRACE(4);
           ++n_tr;
@@ -822,7 +868,6 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
       __syncwarp();
       if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
     }
-    if (t == 0) bulk_wait0();
   }
   tc_teardown(tmem, warp);
 }
@@ -903,6 +948,28 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
     }
   } else if (warp == kWarpMask) {
     mask_loop(p, smem, br, lane);
+  } else if (warp == kWarpStore) {  // ===== TMA stores of staged outputs; stage recycling =====
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int ps = 0; ps < 2; ++ps)
+          for (int c = 0; c < C; ++c, ++it) {
+            const int st = it & 3, g = it & 1;
+            uint8_t* X = smem + kOffRaw + st * kStage;
+            mbar_wait(&br->staged[st], (it >> 2) & 1);
+            if (ps == 0) {
+              tma_store_4d(&tdq, X, 0, c * kRows, h, b);
+            } else {
+              tma_store_4d(&tdk, X, 0, c * kRows, h, b);
+              tma_store_4d(&tdv, X + kTile, 0, c * kRows, h, b);
+            }
+            bulk_wait_read0();
+            mbar_arrive(&br->raw_empty[st]);
+          }
+      }
+      bulk_wait0();
+    }
   } else {  // ===== workers =====
     const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
     const float eps = (float)p.eps;
@@ -920,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
     };
     if (g == 0) fetch_S(blockIdx.x);
     const float qnan = __int_as_float(0x7fc00000);
-    int it = 0, j = 0, prev_st = -1, n_tr = 0;
+    int it = 0, j = 0, n_tr = 0;
     (void)n_tr;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int b = u / H, h = u - b * H;
@@ -949,7 +1016,6 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             load_row32_raw(X + kTile, t, gy);
             inv = rsqrtf(sumsq(xr) + eps);
             scale32(xr, r < N ? inv : 0.f);
-            release_prev(br, prev_st, t);
             split32(xr, h, l);
             store_row32_raw(X, t, h);
             store_row32_raw(Y, t, l);
@@ -984,13 +1050,11 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             f = r < N && flag_at(fl, r);
             inv = rsqrtf(sumsq(xr) + eps);
             scale32(xr, inv);  // padded rows may hold anything: masked below, never multiplied in
-            release_prev(br, prev_st, t);
             tmem_store_split(D + 64, xr, f ? 0xFFFFFFFFu : 0u);
             tmem_store_split(D + 128, vy);
             tmem_wait_st();
             tc_fence_before();
           }
-          prev_st = st;
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&br->split_full[g]);
@@ -1006,51 +1070,47 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             tmem_ld_row(D, gq);
             scale32(gq, uc.s);
             jacobian32(gq, xr, dot32(gq, xr), inv);
+            store_row(X, t, gq);  // staged in the Q tile's slot of the raw stage
+            TC_TRACE(5);
+            arrive_staged(br, st, lane);
             if (c == C - 1) {
               // G complete: dm (:408), dA = s G (:412-413) as both state operands
-              float row[32];
-              const bool own = reduce_rows(tmem, Y + kTile, wq, lane, g, row);
+              float g8[8], h8[8], l8[8];
+              reduce_rows8(tmem, Y + kTile, wq, lane, g, t, g8);
+              const int a = t >> 2, q = t & 3;
               double dot = 0.0;
-              if (own) {
-                const int a = 16 * wq + lane;
-                float sh[32], sl2[32];
-                load_row(ops, a, sh);
-                load_row(ops + kOpBytes, a, sl2);
 #pragma unroll
-                for (int k = 0; k < 32; k += 4) {
-                  float d = row[k] * (sh[k] + sl2[k]);
-                  d = fmaf(row[k + 1], sh[k + 1] + sl2[k + 1], d);
-                  d = fmaf(row[k + 2], sh[k + 2] + sl2[k + 2], d);
-                  d = fmaf(row[k + 3], sh[k + 3] + sl2[k + 3], d);
-                  dot += (double)d;
-                }
-#pragma unroll
-                for (int k = 0; k < 32; ++k) row[k] *= uc.s;  // dA row a
-                float hi[32], lw[32];
-                split_regs(row, hi, lw);
-                store_row(ops + 2 * kOpBytes, a, hi);  // dA rows, K-major B of dK~ = V dA^T
-                store_row(ops + 3 * kOpBytes, a, lw);
-                store_row32(ops + 4 * kOpBytes, a, hi);  // dA rows, MN-major B of dV = K~ dA
-                store_row32(ops + 5 * kOpBytes, a, lw);
+              for (int hh = 0; hh < 2; ++hh) {  // <G, S> (S row a = K-major operand row a)
+                const float4 sh = *reinterpret_cast<const float4*>(ops + chunk_off(a, 2 * q + hh));
+                const float4 sl = *reinterpret_cast<const float4*>(ops + kOpBytes + chunk_off(a, 2 * q + hh));
+                float d = g8[4 * hh] * (sh.x + sl.x);
+                d = fmaf(g8[4 * hh + 1], sh.y + sl.y, d);
+                d = fmaf(g8[4 * hh + 2], sh.z + sl.z, d);
+                d = fmaf(g8[4 * hh + 3], sh.w + sl.w, d);
+                dot += (double)d;
               }
-              // fixed-order dm: 16-lane tree per warp, then warp 0 + warp 1 of the group
 #pragma unroll
-              for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-              if (wq == 1 && lane == 0) *dm_x = dot;
+              for (int k = 0; k < 8; ++k) g8[k] *= uc.s;  // dA row a, columns 8q..8q+7
+              split8(g8, h8, l8);
+              store8_k(ops + 2 * kOpBytes, a, q, h8);  // K-major B of dK~ = V dA^T
+              store8_k(ops + 3 * kOpBytes, a, q, l8);
+              store8_mn(ops + 4 * kOpBytes, a, q, h8);  // MN-major B of dV = K~ dA
+              store8_mn(ops + 5 * kOpBytes, a, q, l8);
+              // fixed-order dm: warp tree, then the 4 warps of the group in order
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+              if (lane == 0) dm_x[wq] = dot;
               fence_proxy_async();
               tc_fence_before();
               group_sync(g);
-              if (t == 0) {
+              if (t == 0) {  // dm partials read before op_ready lets the next unit's G-epilogue run
+                const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
+                if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
                 mbar_arrive(&br->op_ready);
-                if (p.dm_unit) p.dm_unit[u] = uc.coef * (dot + *dm_x);
               }
             } else {
               tc_fence_before();
             }
-            store_row(X, t, gq);  // staged in the Q tile's slot of the raw stage
-            fence_proxy_async();
-            group_sync(g);
-            if (t == 0) tma_store_4d(&tdq, X, 0, c * kRows, h, b);
           } else {
             // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439); dK_i = v_i ? (g - (g.k~)k~)/nk : 0 (:430-437)
             float dv[32], gk[32];
@@ -1067,12 +1127,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             }
             store_row(X, t, gk);
             store_row(X + kTile, t, dv);
-            fence_proxy_async();
-            group_sync(g);
-            if (t == 0) {
-              tma_store_4d(&tdk, X, 0, c * kRows, h, b);
-              tma_store_4d(&tdv, X + kTile, 0, c * kRows, h, b);
-            }
+            TC_TRACE(5);
+            arrive_staged(br, st, lane);
           }
           TC_TRACE(4);
           ++n_tr;
@@ -1080,7 +1136,6 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
       __syncwarp();
       if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
     }
-    if (t == 0) bulk_wait0();
   }
   tc_teardown(tmem, warp);
 }

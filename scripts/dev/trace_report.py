@@ -19,6 +19,9 @@ for tag in ("fwd", "bwd"):
         v = d[..., i][ok]
         print(f"  {n:9s} mean {v.mean():8.0f} cyc  median {np.median(v):8.0f}  p90 {np.percentile(v, 90):8.0f}")
     print(f"  {'gap':9s} mean {gap[okg].mean():8.0f} cyc")
+    w5 = a[:, :2, :, 5]
+    ok5 = ok & (w5 > 0)
+    print(f"  epi before barrier->store {(w5 - w[..., 3])[ok5].mean():8.0f}   store issue {(w[..., 4] - w5)[ok5].mean():8.0f}")
     per_item = (w[:, :, 1:, 0] - w[:, :, :-1, 0])[okg]
     print(f"  item period per group: mean {per_item.mean():.0f} cyc")
     # MMA thread: global item it -> group it&1, group-local index it>>1

@@ -1,7 +1,7 @@
 # tcgen05 bring-up: parity tests for the d32 paths first, then bench both paths.
 mkdir -p gpurun_out
 timeout 300 python scripts/dev/err_table.py > gpurun_out/err_table.txt 2>&1; cat gpurun_out/err_table.txt | tail -12
-timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -15 gpurun_out/pytest_gpu.log
 for path in tcgen05 fp32pipe; do
 for w in ml1m ml20m beauty; do
