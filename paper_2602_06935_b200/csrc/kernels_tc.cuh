@@ -63,7 +63,7 @@ using d32::tma_load_4d;
 constexpr int kRows = 128;                 // rows per chunk
 constexpr uint32_t kTile = 16384;          // 128 rows x 128 B
 constexpr uint32_t kStage = 2 * kTile;     // two tensors per chunk
-constexpr int kRaw = 4;                    // TMA stages
+constexpr int kRing = 3;                   // TMA stages = lo buffers = TMEM buffers
 constexpr int kMaxN = 16384;               // flag bitmask capacity
 constexpr int kGroups = 2;                 // worker groups (alternate chunks)
 constexpr int kWorkerWarps = 4 * kGroups;
@@ -76,8 +76,8 @@ constexpr int kThreads = (kWorkerWarps + 4) * 32;
 
 // Shared-memory plan (bytes; every operand region 1024-aligned for SW128).
 constexpr uint32_t kOffRaw = 0;
-constexpr uint32_t kOffLo = kOffRaw + kRaw * kStage;       // 2 lo buffers
-constexpr uint32_t kOffOps = kOffLo + 2 * kStage;          // 6 x 4 KB state operands
+constexpr uint32_t kOffLo = kOffRaw + kRing * kStage;      // kRing lo buffers
+constexpr uint32_t kOffOps = kOffLo + kRing * kStage;      // 6 x 4 KB state operands
 constexpr uint32_t kOffFlags = kOffOps + 6 * 4096;         // 2 x 2 KB bitmasks
 constexpr uint32_t kOffMisc = kOffFlags + 2 * (kMaxN / 8);  // 2 x 16 B unit constants, tmem base
 constexpr uint32_t kOffBar = kOffMisc + 128;  // misc: UnitConst[2], tmem base, dm partials[4]
@@ -88,16 +88,23 @@ constexpr uint32_t kSmemBytes = kOffBar + 32 * 8;
 // B of dV = K~ dA)
 constexpr uint32_t kOpBytes = 4096;
 
-// TMEM: 512 columns.  Backward: [0, 64) G; group g's buffer at kBwdBuf0 + 192 g:
-// pass 1 [+0, +32) dQ~, [+64, +128) dO hi/lo A operand;
-// pass 2 [+0, +32) dV, [+32, +64) dK~, [+64, +128) K~ hi/lo, [+128, +192) V hi/lo.
+// TMEM: 512 columns.  Backward: [0, 64) G; buffer b at kBwdBuf0 + 128 b:
+// pass 1 [+0, +32) dQ~, [+32, +96) dO hi/lo A operand, [+96, +128) q~;
+// pass 2 [+0, +32) dV, [+32, +64) dK~, [+64, +128) K~ hi/lo A operand
+// (V, the A operand of dK~ = V dA^T, stays in shared memory); the row's
+// 1/norm at column kBwdInv + b (all three splitter -> epiloguer hand-offs).
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kBwdBuf0 = 64;
-constexpr uint32_t kBwdBufCols = 192;
-// Forward: [0, 64) S; group g's buffer at kFwdBuf0 + 96 g: [+0, +32) O,
+constexpr uint32_t kBwdBufCols = 128;
+constexpr uint32_t kBwdInv = kBwdBuf0 + kRing * kBwdBufCols;
+// Forward: [0, 64) S; buffer b at kFwdBuf0 + 96 b: [+0, +32) O,
 // [+32, +96) Q~ hi/lo A operand.
 constexpr uint32_t kFwdBuf0 = 64;
 constexpr uint32_t kFwdBufCols = 96;
+
+// Ring position of item `it` (slot, phase parity); a division by a constant.
+__device__ __forceinline__ int slot3(int it) { return it % kRing; }
+__device__ __forceinline__ uint32_t par3(int it) { return (uint32_t)(it / kRing) & 1u; }
 
 struct UnitConst {  // per flag slot, written by the mask warp
   int tn;
@@ -497,6 +504,21 @@ __device__ __forceinline__ void issue_rowout_ts(uint32_t d, uint32_t ah, uint32_
     mma_tf32_ts(d, ah + 32 + 8 * kk, dh, id, 1u);
   }
 }
+// Same with A = a 128-row chunk in shared memory (K-major, 16-byte granules).
+template <bool kBMN>
+__device__ __forceinline__ void issue_rowout_ss(uint32_t d, uint32_t ah, uint32_t al, uint32_t bh,
+                                                uint32_t bl) {
+  const uint32_t id = idesc_tf32(128, 32, false, kBMN);
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const uint64_t dh = kBMN ? sdesc(bh + 1024u * kk, 4096u, 512u, 1u) : sdesc(bh + 32u * kk, 16u, 1024u);
+    const uint64_t dl = kBMN ? sdesc(bl + 1024u * kk, 4096u, 512u, 1u) : sdesc(bl + 32u * kk, 16u, 1024u);
+    const uint64_t a_h = sdesc(ah + 32u * kk, 16u, 1024u), a_l = sdesc(al + 32u * kk, 16u, 1024u);
+    mma_tf32(d, a_h, dh, id, kk > 0 ? 1u : 0u);
+    mma_tf32(d, a_h, dl, id, 1u);
+    mma_tf32(d, a_l, dh, id, 1u);
+  }
+}
 __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&r)[32]) {
   tmem_ld32(taddr, r);
   tmem_wait_ld();
@@ -512,11 +534,11 @@ __device__ __forceinline__ void tmem_store_split(uint32_t taddr, const float (&x
 }
 
 // ---- optional phase trace (debug builds: -DCOTTEN_TC_TRACE=1) ---------------------
-// Thread 0 of each worker group stamps clock64() at 5 points of its first
-// kTraceItems items: [0] before the TMA wait, [1] data landed, [2] split
-// published, [3] MMAs done, [4] epilogue issued; the MMA thread (slot 2) stamps
-// [0] before its split wait, [1] after it, [2] after issuing, per item.
-// Layout [cta][3][item][8].
+// Per item (first kTraceItems of each CTA), clock64() stamps: splitter thread 0
+// (slot 0): [0] before its waits, [1] stage landed and lo buffer free, [2] split
+// published; epiloguer thread 0 (slot 1): [3] MMAs done, [5] outputs staged,
+// [4] staged barrier arrived; MMA lane 0 (slot 2): [0] before its split wait,
+// [1] after it, [2] after issuing.  Layout [cta][3][item][8].
 #ifndef COTTEN_TC_TRACE
 #define COTTEN_TC_TRACE 0
 #endif
@@ -524,8 +546,8 @@ constexpr int kTraceItems = 64;
 #if COTTEN_TC_TRACE
 #define TC_TRACE(k)                                                                       \
   do {                                                                                    \
-    if (t == 0 && p.workspace && n_tr < kTraceItems)                                     \
-      static_cast<long long*>(p.workspace)[((blockIdx.x * 3 + g) * kTraceItems + n_tr) * 8 + (k)] = \
+    if (t == 0 && p.workspace && it < kTraceItems)                                       \
+      static_cast<long long*>(p.workspace)[((blockIdx.x * 3 + g) * kTraceItems + it) * 8 + (k)] = \
           clock64();                                                                      \
   } while (0)
 #define TC_TRACE_MMA(k)                                                                   \
@@ -546,14 +568,12 @@ constexpr int kTraceItems = 64;
 // ---- warp roles, barriers -------------------------------------------------------
 
 struct Bars {
-  uint64_t raw_full[4], raw_empty[4];  // producer <-> workers (stage = item & 3)
-  uint64_t split_full[2], mma_done[2];  // workers <-> MMA issuer (group = item & 1)
+  // ring slot = item % 3 for the TMA stage, the lo buffer and the TMEM buffer alike
+  uint64_t raw_full[kRing], raw_empty[kRing];  // producer <-> splitter / MMA
+  uint64_t split_full[kRing], mma_done[kRing];  // splitter -> MMA -> epiloguer
   uint64_t op_ready;                    // state operand (S or dA) written, per unit
   uint64_t fl_full[2], fl_empty[2];     // mask warp <-> workers (slot = unit & 1)
-  // workers -> store warp: chunk outputs staged (or none) and the stage's MMAs done.
-  // Indexed by stage, not group: a stage is reloaded only after the store warp
-  // released it, so a group can never complete two phases ahead of the waiter.
-  uint64_t staged[4];
+  uint64_t staged[kRing], lo_free[kRing];  // epiloguer -> store warp -> splitter
 };
 static_assert(sizeof(Bars) <= 256, "barrier area");
 
@@ -565,17 +585,18 @@ __device__ __forceinline__ void group_sync(int g) {
 __device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* tslot, int warp) {
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kRing; ++i) {
       mbar_init(&br->raw_full[i], 1);
       mbar_init(&br->raw_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
       mbar_init(&br->split_full[i], 4);
       mbar_init(&br->mma_done[i], 1);
+      mbar_init(&br->staged[i], 4);
+      mbar_init(&br->lo_free[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&br->fl_full[i], 1);
       mbar_init(&br->fl_empty[i], kWorkerWarps);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&br->staged[i], 4);
     mbar_init(&br->op_ready, 1);
     d32::fence_barrier_init();
   }
@@ -673,10 +694,21 @@ __device__ __forceinline__ void split_regs(const float (&x)[32], float (&h)[32],
 // Arrive on the group's "staged" barrier (one arrival per warp): the chunk's
 // outputs are in its raw stage (or it has none) and the MMAs that read the
 // stage are complete, so the store warp may store it and recycle the stage.
-__device__ __forceinline__ void arrive_staged(Bars* br, int st, int lane) {
+__device__ __forceinline__ void arrive_staged(Bars* br, int b, int lane) {
   fence_proxy_async();
   __syncwarp();
-  if (lane == 0) mbar_arrive(&br->staged[st]);
+  if (lane == 0) mbar_arrive(&br->staged[b]);
+}
+// single-column TMEM store / load (a per-row scalar handed from splitter to epiloguer)
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, float v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr),
+               "r"(__float_as_uint(v))
+               : "memory");
+}
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  return __uint_as_float(v);
 }
 
 // ======================================================================================
@@ -709,8 +741,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
         const int b = u / H, h = u - b * H;
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
-            const int st = it & 3;
-            mbar_wait(&br->raw_empty[st], ((it >> 2) & 1) ^ 1);
+            const int st = slot3(it);
+            mbar_wait(&br->raw_empty[st], par3(it) ^ 1u);
             uint8_t* dst = smem + kOffRaw + st * kStage;
             if (ps == 0) {
               mbar_expect_tx(&br->raw_full[st], 2 * kTile);
@@ -729,61 +761,62 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       for (int ps = 0; ps < P; ++ps)
         for (int c = 0; c < C; ++c, ++it) {
-          const int st = it & 3, g = it & 1;
+          const int st = slot3(it), bf = st;
           TC_TRACE_MMA(0);
-          mbar_wait(&br->split_full[g], (it >> 1) & 1);
+          mbar_wait(&br->split_full[bf], par3(it));
           if (ps == 0 && c == 0 && P == 1 && j > 0)  // previous S read before it is overwritten
             mbar_wait(&br->op_ready, (j - 1) & 1);
           if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
           tc_fence_after();
           TC_TRACE_MMA(1);
           const uint32_t X = base + kOffRaw + st * kStage;
-          const uint32_t Y = base + kOffLo + g * kStage;
+          const uint32_t Y = base + kOffLo + bf * kStage;
           if (elect_one()) {
             if (ps == 0) {  // S += K~^T V (attention.cpp:345-353)
               const int rows = min(kRows, N - c * kRows);
               issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c == 0);
-            } else {  // O = Q~ S (attention.cpp:379-387); B row n = S column n
-              const uint32_t D = tmem + kFwdBuf0 + kFwdBufCols * g;
+            } else {  // O = Q~ S (attention.cpp:379-387), B = S rows (MN-major)
+              const uint32_t D = tmem + kFwdBuf0 + kFwdBufCols * bf;
               issue_rowout_ts<true>(D, D + 32, base + kOffOps, base + kOffOps + kOpBytes);
             }
             TC_TRACE_MMA(2);
-            mma_commit(&br->mma_done[g]);
+            mma_commit(&br->raw_empty[st]);
+            mma_commit(&br->mma_done[bf]);
           }
           __syncwarp();
         }
     }
   } else if (warp == kWarpMask) {
     mask_loop(p, smem, br, lane);
-  } else if (warp == kWarpStore) {  // ===== TMA stores of staged outputs; stage recycling =====
+  } else if (warp == kWarpStore) {  // ===== TMA stores of staged outputs; lo-buffer recycling =====
     if (lane == 0) {
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = u / H, h = u - b * H;
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
-            const int st = it & 3, g = it & 1;
-            mbar_wait(&br->staged[st], (it >> 2) & 1);
+            const int bf = slot3(it);
+            mbar_wait(&br->staged[bf], par3(it));
             if (ps == 1 && p.out) {
-              tma_store_4d(&to, smem + kOffRaw + st * kStage, 0, c * kRows, h, b);
+              tma_store_4d(&to, smem + kOffLo + bf * kStage, 0, c * kRows, h, b);
               bulk_wait_read0();
             }
-            mbar_arrive(&br->raw_empty[st]);
+            mbar_arrive(&br->lo_free[bf]);
           }
       }
       bulk_wait0();
     }
-  } else {  // ===== workers: group g takes items it = g (mod 2); thread t owns chunk row t =====
+  } else {
+    // ===== workers: group 0 splits every chunk, group 1 runs every epilogue;
+    //       thread t owns row t of the chunk (= TMEM lane t) in both =====
     const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
     const float eps = (float)p.eps;
-    float* O = static_cast<float*>(p.out);
     float* norms_all = static_cast<float*>(p.saved_norms);
     float* gS_all = static_cast<float*>(p.saved_S);
     const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
     int it = 0, j = 0, n_tr = 0;
     (void)n_tr;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int b = u / H, h = u - b * H;
       const int sl = j & 1;
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
       float* norms = norms_all ? norms_all + (int64_t)u * 2 * N : nullptr;
@@ -791,79 +824,80 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
       const UnitConst uc = ucs[sl];
       for (int ps = 0; ps < P; ++ps)
         for (int c = 0; c < C; ++c, ++it) {
-          if ((it & 1) != g) continue;
-          const int st = it & 3;
+          const int st = slot3(it), bf = st;
           const int r = c * kRows + t;
           uint8_t* X = smem + kOffRaw + st * kStage;
-          uint8_t* Y = smem + kOffLo + g * kStage;
-          TC_TRACE(0);
-          mbar_wait(&br->raw_full[st], (it >> 2) & 1);
-          TC_TRACE(1);
-          if (ps == 0) {  // K~ (masked, attention.cpp:334-343) and V, 32-byte-granule tiles
-            float kx[32], vx[32], h[32], l[32];
-            load_row32_raw(X, t, kx);  // lane order: only re-stored in the same layout
-            load_row32_raw(X + kTile, t, vx);
-            const bool f = r < N && flag_at(fl, r);
-            const float ss = sumsq(kx) + eps;
-            const float iv = rsqrtf(ss);
-            scale32(kx, iv);
-            if (norms && r < N) norms[N + r] = f ? ss * iv : 1.0f;  // :336, :343
-            split32(kx, h, l, f ? 0xFFFFFFFFu : 0u);  // padded rows: exact zeros, NaN-safe
-            store_row32_raw(X, t, h);
-            store_row32_raw(Y, t, l);
-            split32(vx, h, l);
-            store_row32_raw(X + kTile, t, h);
-            store_row32_raw(Y + kTile, t, l);
-          } else {  // Q~ for every row (attention.cpp:366-377), TMEM A operand of O = Q~ S
-            float qx[32];
-            load_row(X, t, qx);
-            const float ss = sumsq(qx) + eps;
-            const float iv = rsqrtf(ss);
-            scale32(qx, iv);
-            if (norms && r < N) norms[r] = ss * iv;
-            tmem_store_split(tmem + kFwdBuf0 + kFwdBufCols * g + 32 + lane_base, qx);
-            tmem_wait_st();
-            tc_fence_before();
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&br->split_full[g]);
-          TC_TRACE(2);
-
-          // ---- epilogue of this item ----
-          mbar_wait(&br->mma_done[g], (it >> 1) & 1);
-          tc_fence_after();
-          TC_TRACE(3);
-          if (ps == 0) {
-            arrive_staged(br, st, lane);  // no outputs: the stage is free once the MMAs are done
-            if (c == C - 1) {  // S complete: saved S + the MN-major B operand of O = Q~ S
-              float s8[8], h8[8], l8[8];
-              reduce_rows8(tmem, Y + kTile, wq, lane, g, t, s8);
-              const int a = t >> 2, q = t & 3;
-              if (gS_all) {  // coalesced: a warp writes 8 whole rows of S
-                float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024 + a * 32 + 8 * q);
-                gs[0] = make_float4(s8[0], s8[1], s8[2], s8[3]);
-                gs[1] = make_float4(s8[4], s8[5], s8[6], s8[7]);
-              }
-              split8(s8, h8, l8);
-              store8_mn(ops, a, q, h8);
-              store8_mn(ops + kOpBytes, a, q, l8);
-              fence_proxy_async();
+          uint8_t* Y = smem + kOffLo + bf * kStage;
+          const uint32_t D = tmem + kFwdBuf0 + kFwdBufCols * bf + lane_base;
+          if (g == 0) {  // ---------------- splitter ----------------
+            TC_TRACE(0);
+            mbar_wait(&br->raw_full[st], par3(it));
+            mbar_wait(&br->lo_free[bf], par3(it) ^ 1u);
+            TC_TRACE(1);
+            if (ps == 0) {  // K~ (masked, attention.cpp:334-343) and V, 32-byte-granule tiles
+              float kx[32], vx[32], hh[32], ll[32];
+              load_row32_raw(X, t, kx);  // lane order: only re-stored in the same layout
+              load_row32_raw(X + kTile, t, vx);
+              const bool f = r < N && flag_at(fl, r);
+              const float ss = sumsq(kx) + eps;
+              const float iv = rsqrtf(ss);
+              scale32(kx, iv);
+              if (norms && r < N) norms[N + r] = f ? ss * iv : 1.0f;  // :336, :343
+              split32(kx, hh, ll, f ? 0xFFFFFFFFu : 0u);  // padded rows: exact zeros, NaN-safe
+              store_row32_raw(X, t, hh);
+              store_row32_raw(Y, t, ll);
+              split32(vx, hh, ll);
+              store_row32_raw(X + kTile, t, hh);
+              store_row32_raw(Y + kTile, t, ll);
+            } else {  // Q~ for every row (attention.cpp:366-377), TMEM A operand of O = Q~ S
+              float qx[32];
+              load_row(X, t, qx);
+              const float ss = sumsq(qx) + eps;
+              const float iv = rsqrtf(ss);
+              scale32(qx, iv);
+              if (norms && r < N) norms[r] = ss * iv;
+              tmem_store_split(D + 32, qx);
+              tmem_wait_st();
               tc_fence_before();
-              group_sync(g);
-              if (t == 0) mbar_arrive(&br->op_ready);
             }
-          } else {  // O rows = s (Q~ S) (attention.cpp:379-387), staged in the raw stage
-            float acc[32];
-            tmem_ld_row(tmem + kFwdBuf0 + kFwdBufCols * g + lane_base, acc);
-            tc_fence_before();
-            scale32(acc, uc.s);
-            store_row(X, t, acc);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&br->split_full[bf]);
+            TC_TRACE(2);
+          } else {  // ---------------- epiloguer ----------------
+            mbar_wait(&br->mma_done[bf], par3(it));
+            tc_fence_after();
+            TC_TRACE(3);
+            if (ps == 0) {
+              if (c == C - 1) {  // S complete: saved S + the MN-major B operand of O = Q~ S
+                float s8[8], h8[8], l8[8];
+                reduce_rows8(tmem, Y + kTile, wq, lane, g, t, s8);
+                const int a = t >> 2, q = t & 3;
+                if (gS_all) {  // coalesced: a warp writes 8 whole rows of S
+                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024 + a * 32 + 8 * q);
+                  gs[0] = make_float4(s8[0], s8[1], s8[2], s8[3]);
+                  gs[1] = make_float4(s8[4], s8[5], s8[6], s8[7]);
+                }
+                split8(s8, h8, l8);
+                store8_mn(ops, a, q, h8);
+                store8_mn(ops + kOpBytes, a, q, l8);
+                fence_proxy_async();
+                tc_fence_before();
+                group_sync(g);
+                if (t == 0) mbar_arrive(&br->op_ready);
+              }
+            } else {  // O rows = s (Q~ S) (attention.cpp:379-387), staged in the lo buffer
+              float acc[32];
+              tmem_ld_row(D, acc);
+              tc_fence_before();
+              scale32(acc, uc.s);
+              store_row(Y, t, acc);
+            }
             TC_TRACE(5);
-            arrive_staged(br, st, lane);
+            arrive_staged(br, bf, lane);
+            TC_TRACE(4);
+            ++n_tr;
           }
-          TC_TRACE(4);
-          ++n_tr;
         }
       __syncwarp();
       if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
@@ -902,8 +936,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
         const int b = u / H, h = u - b * H;
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
-            const int st = it & 3;
-            mbar_wait(&br->raw_empty[st], ((it >> 2) & 1) ^ 1);
+            const int st = slot3(it);
+            mbar_wait(&br->raw_empty[st], par3(it) ^ 1u);
             uint8_t* dst = smem + kOffRaw + st * kStage;
             mbar_expect_tx(&br->raw_full[st], 2 * kTile);
             tma_load_4d(dst, ps == 0 ? &tq : &tk, 0, c * kRows, h, b, &br->raw_full[st]);
@@ -918,65 +952,66 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       for (int ps = 0; ps < 2; ++ps)
         for (int c = 0; c < C; ++c, ++it) {
-          const int st = it & 3, g = it & 1;
+          const int st = slot3(it), bf = st;
           TC_TRACE_MMA(0);
-          mbar_wait(&br->split_full[g], (it >> 1) & 1);
+          mbar_wait(&br->split_full[bf], par3(it));
           if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
           tc_fence_after();
           TC_TRACE_MMA(1);
           const uint32_t X = base + kOffRaw + st * kStage;
-          const uint32_t Y = base + kOffLo + g * kStage;
-          const uint32_t D = tmem + kBwdBuf0 + kBwdBufCols * g;
+          const uint32_t Y = base + kOffLo + bf * kStage;
+          const uint32_t D = tmem + kBwdBuf0 + kBwdBufCols * bf;
           if (elect_one()) {
             if (ps == 0) {
               // G += Q~^T dO (attention.cpp:405)
               const int rows = min(kRows, N - c * kRows);
               issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c == 0);
               // dQ~ (unscaled) = dO S^T (:410-411): A = dO hi/lo in TMEM, B row n = S row n
-              issue_rowout_ts<false>(D, D + 64, opS, opS + kOpBytes);
+              issue_rowout_ts<false>(D, D + 32, opS, opS + kOpBytes);
             } else {
-              // dV = K~ dA (:416): B = dA row-major as an MN-major operand
+              // dV = K~ dA (:416): A = K~ hi/lo in TMEM, B = dA rows as an MN-major operand
               issue_rowout_ts<true>(D, D + 64, opAt, opAt + kOpBytes);
-              // dK~ = V dA^T (:415): B row n = dA row n (K-major)
-              issue_rowout_ts<false>(D + 32, D + 128, opA, opA + kOpBytes);
+              // dK~ = V dA^T (:415): A = V hi (TMA stage) / lo (lo buffer), B row n = dA row n
+              issue_rowout_ss<false>(D + 32, X + kTile, Y + kTile, opA, opA + kOpBytes);
             }
             TC_TRACE_MMA(2);
-            mma_commit(&br->mma_done[g]);
+            mma_commit(&br->raw_empty[st]);
+            mma_commit(&br->mma_done[bf]);
           }
           __syncwarp();
         }
     }
   } else if (warp == kWarpMask) {
     mask_loop(p, smem, br, lane);
-  } else if (warp == kWarpStore) {  // ===== TMA stores of staged outputs; stage recycling =====
+  } else if (warp == kWarpStore) {  // ===== TMA stores of staged outputs; lo-buffer recycling =====
     if (lane == 0) {
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = u / H, h = u - b * H;
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
-            const int st = it & 3, g = it & 1;
-            uint8_t* X = smem + kOffRaw + st * kStage;
-            mbar_wait(&br->staged[st], (it >> 2) & 1);
+            const int bf = slot3(it);
+            uint8_t* Y = smem + kOffLo + bf * kStage;
+            mbar_wait(&br->staged[bf], par3(it));
             if (ps == 0) {
-              tma_store_4d(&tdq, X, 0, c * kRows, h, b);
+              tma_store_4d(&tdq, Y, 0, c * kRows, h, b);
             } else {
-              tma_store_4d(&tdk, X, 0, c * kRows, h, b);
-              tma_store_4d(&tdv, X + kTile, 0, c * kRows, h, b);
+              tma_store_4d(&tdk, Y, 0, c * kRows, h, b);
+              tma_store_4d(&tdv, Y + kTile, 0, c * kRows, h, b);
             }
             bulk_wait_read0();
-            mbar_arrive(&br->raw_empty[st]);
+            mbar_arrive(&br->lo_free[bf]);
           }
       }
       bulk_wait0();
     }
-  } else {  // ===== workers =====
+  } else {
+    // ===== workers: group 0 splits every chunk, group 1 runs every epilogue =====
     const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
     const float eps = (float)p.eps;
     const float* gS_all = static_cast<const float*>(p.saved_S);
     const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
-    // saved S of the group's next unit-start item, prefetched a unit ahead
-    // (group 0 always owns chunk 0 of pass 1: units have an even item count)
+    // saved S of the next unit, prefetched a unit ahead by the splitter
     float4 snext[2];
     auto fetch_S = [&](int u) {
       if (u < units) {
@@ -990,148 +1025,161 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
     int it = 0, j = 0, n_tr = 0;
     (void)n_tr;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int b = u / H, h = u - b * H;
       const int sl = j & 1;
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
       mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
       const UnitConst uc = ucs[sl];
       for (int ps = 0; ps < 2; ++ps)
         for (int c = 0; c < C; ++c, ++it) {
-          if ((it & 1) != g) continue;
-          const int st = it & 3;
+          const int st = slot3(it), bf = st;
           const int r = c * kRows + t;
           uint8_t* X = smem + kOffRaw + st * kStage;
-          uint8_t* Y = smem + kOffLo + g * kStage;
-          const uint32_t D = tmem + kBwdBuf0 + kBwdBufCols * g + lane_base;
-          TC_TRACE(0);
-          mbar_wait(&br->raw_full[st], (it >> 2) & 1);
-          TC_TRACE(1);
-          float xr[32], inv;
-          bool f = true;
-          if (ps == 0) {
-            // Q~ every row (:366-377, used again in :421-428); rows past N are exact
-            // zeros in G even for eps = 0.  Tiles use the 32-byte-granule swizzle.
-            float gy[32], h[32], l[32];
-            load_row32_raw(X, t, xr);
-            load_row32_raw(X + kTile, t, gy);
-            inv = rsqrtf(sumsq(xr) + eps);
-            scale32(xr, r < N ? inv : 0.f);
-            split32(xr, h, l);
-            store_row32_raw(X, t, h);
-            store_row32_raw(Y, t, l);
-            unswap32(xr, t);  // natural order: the dQ Jacobian pairs it with TMEM columns
-            split32(gy, h, l);
-            store_row32_raw(X + kTile, t, h);
-            store_row32_raw(Y + kTile, t, l);
-            unswap32(h, t);  // dO as the TMEM A operand of dQ~ = dO S^T
-            unswap32(l, t);
-            tmem_st32(D + 64, h);
-            tmem_st32(D + 96, l);
-            if (c == 0) {  // S rows (row n = S row n) for dQ~ = dO S^T
+          uint8_t* Y = smem + kOffLo + bf * kStage;
+          const uint32_t D = tmem + kBwdBuf0 + kBwdBufCols * bf + lane_base;
+          const uint32_t tinv = tmem + kBwdInv + bf + lane_base;
+          if (g == 0) {  // ---------------- splitter ----------------
+            TC_TRACE(0);
+            mbar_wait(&br->raw_full[st], par3(it));
+            mbar_wait(&br->lo_free[bf], par3(it) ^ 1u);
+            TC_TRACE(1);
+            if (ps == 0) {
+              // Q~ every row (:366-377, used again in :421-428); rows past N are exact
+              // zeros in G even for eps = 0.  Tiles use the 32-byte-granule swizzle.
+              float xr[32], hh[32], ll[32];
+              load_row32_raw(X, t, xr);
+              const float inv = rsqrtf(sumsq(xr) + eps);
+              scale32(xr, r < N ? inv : 0.f);
+              split32(xr, hh, ll);
+              store_row32_raw(X, t, hh);
+              store_row32_raw(Y, t, ll);
+              unswap32(xr, t);  // q~ and inv for the epiloguer's dQ Jacobian
+              tmem_st32(D + 96, xr);
+              tmem_st1(tinv, inv);
+              load_row32_raw(X + kTile, t, xr);  // dO
+              split32(xr, hh, ll);
+              store_row32_raw(X + kTile, t, hh);
+              store_row32_raw(Y + kTile, t, ll);
+              unswap32(hh, t);  // dO as the TMEM A operand of dQ~ = dO S^T
+              unswap32(ll, t);
+              tmem_st32(D + 32, hh);
+              tmem_st32(D + 64, ll);
+              if (c == 0) {  // S rows (row n = S row n) for dQ~ = dO S^T
 #pragma unroll
-              for (int e2 = 0; e2 < 2; ++e2) {
-                const int e = t + 128 * e2;
-                const int n = e >> 3, q4 = e & 7;
-                const float4 v = snext[e2];
-                const float4 hq = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-                *reinterpret_cast<float4*>(ops + chunk_off(n, q4)) = hq;
-                *reinterpret_cast<float4*>(ops + kOpBytes + chunk_off(n, q4)) =
-                    make_float4(tf32_lo(v.x, hq.x), tf32_lo(v.y, hq.y), tf32_lo(v.z, hq.z),
-                                tf32_lo(v.w, hq.w));
+                for (int e2 = 0; e2 < 2; ++e2) {
+                  const int e = t + 128 * e2;
+                  const int n = e >> 3, q4 = e & 7;
+                  const float4 v = snext[e2];
+                  const float4 hq =
+                      make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                  *reinterpret_cast<float4*>(ops + chunk_off(n, q4)) = hq;
+                  *reinterpret_cast<float4*>(ops + kOpBytes + chunk_off(n, q4)) =
+                      make_float4(tf32_lo(v.x, hq.x), tf32_lo(v.y, hq.y), tf32_lo(v.z, hq.z),
+                                  tf32_lo(v.w, hq.w));
+                }
+                fetch_S(u + gridDim.x);
               }
-              fetch_S(u + gridDim.x);
+            } else {  // K~ masked (TMEM A operand of dV = K~ dA) and V (smem A of dK~ = V dA^T)
+              float kx[32];
+              load_row(X, t, kx);
+              const bool f = r < N && flag_at(fl, r);
+              const float inv = rsqrtf(sumsq(kx) + eps);
+              scale32(kx, inv);  // padded rows may hold anything: masked, never multiplied in
+              tmem_store_split(D + 64, kx, f ? 0xFFFFFFFFu : 0u);
+              tmem_st1(tinv, inv);
+              load_row(X + kTile, t, kx);  // V
+              store_split(X + kTile, Y + kTile, t, kx);
             }
             tmem_wait_st();
             tc_fence_before();
-          } else {  // K~ masked (:334-343) and V: TMEM A operands of dV = K~ dA, dK~ = V dA^T
-            float vy[32];
-            load_row(X, t, xr);
-            load_row(X + kTile, t, vy);
-            f = r < N && flag_at(fl, r);
-            inv = rsqrtf(sumsq(xr) + eps);
-            scale32(xr, inv);  // padded rows may hold anything: masked below, never multiplied in
-            tmem_store_split(D + 64, xr, f ? 0xFFFFFFFFu : 0u);
-            tmem_store_split(D + 128, vy);
-            tmem_wait_st();
-            tc_fence_before();
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&br->split_full[g]);
-          TC_TRACE(2);
-
-          // ---- epilogue of this item ----
-          mbar_wait(&br->mma_done[g], (it >> 1) & 1);
-          tc_fence_after();
-          TC_TRACE(3);
-          if (ps == 0) {
-            // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428)
-            float gq[32];
-            tmem_ld_row(D, gq);
-            scale32(gq, uc.s);
-            jacobian32(gq, xr, dot32(gq, xr), inv);
-            store_row(X, t, gq);  // staged in the Q tile's slot of the raw stage
-            TC_TRACE(5);
-            arrive_staged(br, st, lane);
-            if (c == C - 1) {
-              // G complete: dm (:408), dA = s G (:412-413) as both state operands
-              float g8[8], h8[8], l8[8];
-              reduce_rows8(tmem, Y + kTile, wq, lane, g, t, g8);
-              const int a = t >> 2, q = t & 3;
-              double dot = 0.0;
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&br->split_full[bf]);
+            TC_TRACE(2);
+          } else {  // ---------------- epiloguer ----------------
+            mbar_wait(&br->mma_done[bf], par3(it));
+            tc_fence_after();
+            TC_TRACE(3);
+            if (ps == 0) {
+              // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428)
+              float gq[32], xq[32];
+              tmem_ld32(D, gq);
+              tmem_ld32(D + 96, xq);
+              const float inv = tmem_ld1(tinv);
+              tmem_wait_ld();
+              scale32(gq, uc.s);
+              jacobian32(gq, xq, dot32(gq, xq), inv);
+              store_row(Y, t, gq);  // staged in the lo buffer (free: the MMAs are done)
+              if (c == C - 1) {
+                // G complete: dm (:408), dA = s G (:412-413) as both state operands
+                float g8[8], h8[8], l8[8];
+                reduce_rows8(tmem, Y + kTile, wq, lane, g, t, g8);
+                const int a = t >> 2, q = t & 3;
+                double dot = 0.0;
 #pragma unroll
-              for (int hh = 0; hh < 2; ++hh) {  // <G, S> (S row a = K-major operand row a)
-                const float4 sh = *reinterpret_cast<const float4*>(ops + chunk_off(a, 2 * q + hh));
-                const float4 sl = *reinterpret_cast<const float4*>(ops + kOpBytes + chunk_off(a, 2 * q + hh));
-                float d = g8[4 * hh] * (sh.x + sl.x);
-                d = fmaf(g8[4 * hh + 1], sh.y + sl.y, d);
-                d = fmaf(g8[4 * hh + 2], sh.z + sl.z, d);
-                d = fmaf(g8[4 * hh + 3], sh.w + sl.w, d);
-                dot += (double)d;
-              }
+                for (int hh2 = 0; hh2 < 2; ++hh2) {  // <G, S> (S row a = K-major operand row a)
+                  const float4 sh = *reinterpret_cast<const float4*>(ops + chunk_off(a, 2 * q + hh2));
+                  const float4 sl4 =
+                      *reinterpret_cast<const float4*>(ops + kOpBytes + chunk_off(a, 2 * q + hh2));
+                  float d = g8[4 * hh2] * (sh.x + sl4.x);
+                  d = fmaf(g8[4 * hh2 + 1], sh.y + sl4.y, d);
+                  d = fmaf(g8[4 * hh2 + 2], sh.z + sl4.z, d);
+                  d = fmaf(g8[4 * hh2 + 3], sh.w + sl4.w, d);
+                  dot += (double)d;
+                }
 #pragma unroll
-              for (int k = 0; k < 8; ++k) g8[k] *= uc.s;  // dA row a, columns 8q..8q+7
-              split8(g8, h8, l8);
-              store8_k(ops + 2 * kOpBytes, a, q, h8);  // K-major B of dK~ = V dA^T
-              store8_k(ops + 3 * kOpBytes, a, q, l8);
-              store8_mn(ops + 4 * kOpBytes, a, q, h8);  // MN-major B of dV = K~ dA
-              store8_mn(ops + 5 * kOpBytes, a, q, l8);
-              // fixed-order dm: warp tree, then the 4 warps of the group in order
+                for (int k = 0; k < 8; ++k) g8[k] *= uc.s;  // dA row a, columns 8q..8q+7
+                split8(g8, h8, l8);
+                store8_k(ops + 2 * kOpBytes, a, q, h8);  // K-major B of dK~ = V dA^T
+                store8_k(ops + 3 * kOpBytes, a, q, l8);
+                store8_mn(ops + 4 * kOpBytes, a, q, h8);  // MN-major B of dV = K~ dA
+                store8_mn(ops + 5 * kOpBytes, a, q, l8);
+                // fixed-order dm: warp tree, then the 4 warps of the group in order
 #pragma unroll
-              for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-              if (lane == 0) dm_x[wq] = dot;
-              fence_proxy_async();
-              tc_fence_before();
-              group_sync(g);
-              if (t == 0) {  // dm partials read before op_ready lets the next unit's G-epilogue run
-                const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
-                if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
-                mbar_arrive(&br->op_ready);
+                for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                if (lane == 0) dm_x[wq] = dot;
+                fence_proxy_async();
+                tc_fence_before();
+                group_sync(g);
+                if (t == 0) {  // dm partials read before op_ready lets the next G-epilogue run
+                  const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
+                  if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
+                  mbar_arrive(&br->op_ready);
+                }
+              } else {
+                tc_fence_before();
               }
             } else {
+              // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439); dK_i = v_i ? (g - (g.k~)k~)/nk : 0 (:430-437)
+              float dv[32], gk[32], kx[32], kl[32];
+              tmem_ld32(D, dv);
+              tmem_ld32(D + 32, gk);
+              tmem_ld32(D + 64, kx);
+              tmem_ld32(D + 96, kl);
+              const float inv = tmem_ld1(tinv);
+              tmem_wait_ld();
               tc_fence_before();
-            }
-          } else {
-            // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439); dK_i = v_i ? (g - (g.k~)k~)/nk : 0 (:430-437)
-            float dv[32], gk[32];
-            tmem_ld32(D, dv);
-            tmem_ld32(D + 32, gk);
-            tmem_wait_ld();
-            tc_fence_before();
-            jacobian32(gk, xr, dot32(gk, xr), inv);
-            keep_if(dv, f);  // padded rows: exact zeros (:437, :439)
-            keep_if(gk, f);
-            if (uc.tn == 0) {  // UsageError in the reference: NaN outputs + status bit
+              const bool f = r < N && flag_at(fl, r);
 #pragma unroll
-              for (int k = 0; k < 32; ++k) dv[k] = gk[k] = qnan;
+              for (int k = 0; k < 32; k += 2) {  // k~ = hi + lo exactly (valid rows)
+                const float2 v = __fadd2_rn(f2p(kx[k], kx[k + 1]), f2p(kl[k], kl[k + 1]));
+                kx[k] = v.x;
+                kx[k + 1] = v.y;
+              }
+              jacobian32(gk, kx, dot32(gk, kx), inv);
+              keep_if(dv, f);  // padded rows: exact zeros (:437, :439)
+              keep_if(gk, f);
+              if (uc.tn == 0) {  // UsageError in the reference: NaN outputs + status bit
+#pragma unroll
+                for (int k = 0; k < 32; ++k) dv[k] = gk[k] = qnan;
+              }
+              store_row(Y, t, gk);
+              store_row(Y + kTile, t, dv);
             }
-            store_row(X, t, gk);
-            store_row(X + kTile, t, dv);
             TC_TRACE(5);
-            arrive_staged(br, st, lane);
+            arrive_staged(br, bf, lane);
+            TC_TRACE(4);
+            ++n_tr;
           }
-          TC_TRACE(4);
-          ++n_tr;
         }
       __syncwarp();
       if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
