@@ -401,6 +401,28 @@ __device__ __forceinline__ void store_row32_raw(uint8_t* tile, int row, const fl
         make_float4(x[8 * q + 4], x[8 * q + 5], x[8 * q + 6], x[8 * q + 7]);
   }
 }
+// Natural column order, no selects, 2-way bank conflicts (rows r and r+4 of a
+// warp share granule positions).  COTTEN_TC_P1_NATURAL picks this for the
+// backward's pass-1 tiles, whose rows are needed in natural order anyway.
+#ifndef COTTEN_TC_P1_NATURAL
+#define COTTEN_TC_P1_NATURAL 0
+#endif
+__device__ __forceinline__ void load_row32_nat(const uint8_t* tile, int row, float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = *reinterpret_cast<const float4*>(tile + chunk_off32(row, j));
+    x[4 * j] = v.x;
+    x[4 * j + 1] = v.y;
+    x[4 * j + 2] = v.z;
+    x[4 * j + 3] = v.w;
+  }
+}
+__device__ __forceinline__ void store_row32_nat(uint8_t* tile, int row, const float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(tile + chunk_off32(row, j)) =
+        make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+}
 // lane order -> natural column order (and back: the map is an involution)
 __device__ __forceinline__ void unswap32(float (&x)[32], int row) {
   const bool s = (row >> 2) & 1;
@@ -822,8 +844,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
       float* norms = norms_all ? norms_all + (int64_t)u * 2 * N : nullptr;
       mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
       const UnitConst uc = ucs[sl];
-      for (int ps = 0; ps < P; ++ps)
-        for (int c = 0; c < C; ++c, ++it) {
+      for (int k = 0; k < P * C; ++k, ++it) {  // the unit's chunks: pass 1, then pass 2
+          const int ps = k >= C, c = ps ? k - C : k;
           const int st = slot3(it), bf = st;
           const int r = c * kRows + t;
           uint8_t* X = smem + kOffRaw + st * kStage;
@@ -1029,8 +1051,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
       mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
       const UnitConst uc = ucs[sl];
-      for (int ps = 0; ps < 2; ++ps)
-        for (int c = 0; c < C; ++c, ++it) {
+      for (int k = 0; k < 2 * C; ++k, ++it) {  // the unit's chunks: pass 1, then pass 2
+          const int ps = k >= C, c = ps ? k - C : k;
           const int st = slot3(it), bf = st;
           const int r = c * kRows + t;
           uint8_t* X = smem + kOffRaw + st * kStage;
@@ -1046,22 +1068,38 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               // Q~ every row (:366-377, used again in :421-428); rows past N are exact
               // zeros in G even for eps = 0.  Tiles use the 32-byte-granule swizzle.
               float xr[32], hh[32], ll[32];
+#if COTTEN_TC_P1_NATURAL
+              load_row32_nat(X, t, xr);
+#else
               load_row32_raw(X, t, xr);
+#endif
               const float inv = rsqrtf(sumsq(xr) + eps);
               scale32(xr, r < N ? inv : 0.f);
               split32(xr, hh, ll);
+#if COTTEN_TC_P1_NATURAL
+              store_row32_nat(X, t, hh);
+              store_row32_nat(Y, t, ll);
+#else
               store_row32_raw(X, t, hh);
               store_row32_raw(Y, t, ll);
-              unswap32(xr, t);  // q~ and inv for the epiloguer's dQ Jacobian
-              tmem_st32(D + 96, xr);
+              unswap32(xr, t);  // natural order: the dQ Jacobian pairs it with TMEM columns
+#endif
+              tmem_st32(D + 96, xr);  // q~ and inv for the epiloguer's dQ Jacobian
               tmem_st1(tinv, inv);
+#if COTTEN_TC_P1_NATURAL
+              load_row32_nat(X + kTile, t, xr);  // dO
+              split32(xr, hh, ll);
+              store_row32_nat(X + kTile, t, hh);
+              store_row32_nat(Y + kTile, t, ll);
+#else
               load_row32_raw(X + kTile, t, xr);  // dO
               split32(xr, hh, ll);
               store_row32_raw(X + kTile, t, hh);
               store_row32_raw(Y + kTile, t, ll);
-              unswap32(hh, t);  // dO as the TMEM A operand of dQ~ = dO S^T
+              unswap32(hh, t);
               unswap32(ll, t);
-              tmem_st32(D + 32, hh);
+#endif
+              tmem_st32(D + 32, hh);  // dO as the TMEM A operand of dQ~ = dO S^T
               tmem_st32(D + 64, ll);
               if (c == 0) {  // S rows (row n = S row n) for dQ~ = dO S^T
 #pragma unroll
@@ -1150,30 +1188,41 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               }
             } else {
               // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439); dK_i = v_i ? (g - (g.k~)k~)/nk : 0 (:430-437)
-              float dv[32], gk[32], kx[32], kl[32];
-              tmem_ld32(D, dv);
-              tmem_ld32(D + 32, gk);
-              tmem_ld32(D + 64, kx);
-              tmem_ld32(D + 96, kl);
-              const float inv = tmem_ld1(tinv);
-              tmem_wait_ld();
-              tc_fence_before();
               const bool f = r < N && flag_at(fl, r);
+              const bool nan_out = uc.tn == 0;  // UsageError in the reference: NaN + status bit
+              float kx[32], gk[32];
+              float inv;
+              {  // k~ = hi + lo exactly (valid rows); staged loads keep the register peak low
+                float kl[32];
+                tmem_ld32(D + 64, kx);
+                tmem_ld32(D + 96, kl);
+                inv = tmem_ld1(tinv);
+                tmem_wait_ld();
 #pragma unroll
-              for (int k = 0; k < 32; k += 2) {  // k~ = hi + lo exactly (valid rows)
-                const float2 v = __fadd2_rn(f2p(kx[k], kx[k + 1]), f2p(kl[k], kl[k + 1]));
-                kx[k] = v.x;
-                kx[k + 1] = v.y;
+                for (int k = 0; k < 32; k += 2) {
+                  const float2 v = __fadd2_rn(f2p(kx[k], kx[k + 1]), f2p(kl[k], kl[k + 1]));
+                  kx[k] = v.x;
+                  kx[k + 1] = v.y;
+                }
               }
+              tmem_ld32(D + 32, gk);
+              tmem_wait_ld();
               jacobian32(gk, kx, dot32(gk, kx), inv);
-              keep_if(dv, f);  // padded rows: exact zeros (:437, :439)
-              keep_if(gk, f);
-              if (uc.tn == 0) {  // UsageError in the reference: NaN outputs + status bit
+              keep_if(gk, f);  // padded rows: exact zeros (:437)
+              if (nan_out) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) dv[k] = gk[k] = qnan;
+                for (int k = 0; k < 32; ++k) gk[k] = qnan;
               }
               store_row(Y, t, gk);
-              store_row(Y + kTile, t, dv);
+              tmem_ld32(D, gk);  // dV
+              tmem_wait_ld();
+              tc_fence_before();
+              keep_if(gk, f);  // (:439)
+              if (nan_out) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) gk[k] = qnan;
+              }
+              store_row(Y + kTile, t, gk);
             }
             TC_TRACE(5);
             arrive_staged(br, bf, lane);
