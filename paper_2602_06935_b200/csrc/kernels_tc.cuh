@@ -65,6 +65,10 @@ constexpr uint32_t kTile = 16384;          // 128 rows x 128 B
 constexpr uint32_t kStage = 2 * kTile;     // two tensors per chunk
 constexpr int kRing = 3;                   // TMA stages = lo buffers = TMEM buffers
 constexpr int kMaxN = 16384;               // flag bitmask capacity
+// The S / G reduction accumulator is flushed into an fp32 running sum every
+// kFlush chunks (512 rows), so no TMEM accumulation chain exceeds 64 MMA steps
+// whatever N is (accuracy of long sequences; a no-op for N <= 512).
+constexpr int kFlush = 4;
 constexpr int kGroups = 2;                 // worker groups (alternate chunks)
 constexpr int kWorkerWarps = 4 * kGroups;
 constexpr int kWarpProducer = kWorkerWarps;
@@ -594,6 +598,7 @@ struct Bars {
   uint64_t raw_full[kRing], raw_empty[kRing];  // producer <-> splitter / MMA
   uint64_t split_full[kRing], mma_done[kRing];  // splitter -> MMA -> epiloguer
   uint64_t op_ready;                    // state operand (S or dA) written, per unit
+  uint64_t acc_free;                    // epiloguer flushed the reduction accumulator
   uint64_t fl_full[2], fl_empty[2];     // mask warp <-> workers (slot = unit & 1)
   uint64_t staged[kRing], lo_free[kRing];  // epiloguer -> store warp -> splitter
 };
@@ -620,6 +625,7 @@ __device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* 
       mbar_init(&br->fl_empty[i], kWorkerWarps);
     }
     mbar_init(&br->op_ready, 1);
+    mbar_init(&br->acc_free, 4);
     d32::fence_barrier_init();
   }
   if (warp == kWarpMma) {
@@ -662,7 +668,8 @@ __device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars
 // products, spread over the whole group: thread t gets row a = t/4, columns
 // [8(t%4), 8(t%4)+8).  scratch: 8 KB of free smem (two 32-row partial tiles).
 __device__ __forceinline__ void reduce_rows8(uint32_t tmem, uint8_t* scratch, int wq, int lane,
-                                             int g, int t, float (&r8)[8]) {
+                                             int g, int t, float (&r8)[8],
+                                             const uint8_t* run = nullptr) {
   float a[32], c[32];
   const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16);
   tmem_ld32(ta, a);
@@ -683,6 +690,37 @@ __device__ __forceinline__ void reduce_rows8(uint32_t tmem, uint8_t* scratch, in
     r8[4 * h + 1] = u.y + v.y;
     r8[4 * h + 2] = u.z + v.z;
     r8[4 * h + 3] = u.w + v.w;
+    if (run) {  // + the flushed partial sums of earlier chunks (same tile layout)
+      const float4 x = *reinterpret_cast<const float4*>(run + chunk_off(ra, 2 * q + h));
+      const float4 y = *reinterpret_cast<const float4*>(run + 4096 + chunk_off(ra, 2 * q + h));
+      r8[4 * h + 0] += x.x + y.x;
+      r8[4 * h + 1] += x.y + y.y;
+      r8[4 * h + 2] += x.z + y.z;
+      r8[4 * h + 3] += x.w + y.w;
+    }
+  }
+  if (run) group_sync(g);  // the running sum is read before its area is reused
+}
+// Flush the reduction accumulator into the running sum (two 32-row tiles:
+// x_hi rows, x_lo rows; each lane < 16 owns one row, so no synchronisation).
+__device__ __forceinline__ void flush_acc(uint32_t tmem, uint8_t* run, int wq, int lane,
+                                          bool first) {
+  float a[32], c[32];
+  const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16);
+  tmem_ld32(ta, a);
+  tmem_ld32(ta + 32, c);
+  tmem_wait_ld();
+  if (lane < 16) {
+    uint8_t* tile = run + (wq >> 1) * 4096;
+    const int row = 16 * (wq & 1) + lane;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) a[k] += c[k];
+    if (!first) {
+      load_row(tile, row, c);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) a[k] += c[k];
+    }
+    store_row(tile, row, a);
   }
 }
 // 8 columns [8q, 8q+8) of row a as hi / lo into a K-major (16-byte granule)
@@ -778,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
       }
     }
   } else if (warp == kWarpMma) {  // ===== MMA issuer (whole warp, one elected lane issues) =====
-    int it = 0, j = 0;
+    int it = 0, j = 0, nflush = 0;
     const uint32_t base = smem_u32(smem);
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       for (int ps = 0; ps < P; ++ps)
@@ -788,6 +826,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
           mbar_wait(&br->split_full[bf], par3(it));
           if (ps == 0 && c == 0 && P == 1 && j > 0)  // previous S read before it is overwritten
             mbar_wait(&br->op_ready, (j - 1) & 1);
+          if (ps == 0 && c > 0 && c % kFlush == 0) mbar_wait(&br->acc_free, (nflush++) & 1);
           if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
           tc_fence_after();
           TC_TRACE_MMA(1);
@@ -796,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
           if (elect_one()) {
             if (ps == 0) {  // S += K~^T V (attention.cpp:345-353)
               const int rows = min(kRows, N - c * kRows);
-              issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c == 0);
+              issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c % kFlush == 0);
             } else {  // O = Q~ S (attention.cpp:379-387), B = S rows (MN-major)
               const uint32_t D = tmem + kFwdBuf0 + kFwdBufCols * bf;
               issue_rowout_ts<true>(D, D + 32, base + kOffOps, base + kOffOps + kOpBytes);
@@ -891,9 +930,16 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
             tc_fence_after();
             TC_TRACE(3);
             if (ps == 0) {
+              uint8_t* run = ops + 2 * kOpBytes;  // 8 KB the forward does not otherwise use
+              if (c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
+                flush_acc(tmem, run, wq, lane, c == kFlush - 1);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&br->acc_free);
+              }
               if (c == C - 1) {  // S complete: saved S + the MN-major B operand of O = Q~ S
                 float s8[8], h8[8], l8[8];
-                reduce_rows8(tmem, Y + kTile, wq, lane, g, t, s8);
+                reduce_rows8(tmem, Y + kTile, wq, lane, g, t, s8, C > kFlush ? run : nullptr);
                 const int a = t >> 2, q = t & 3;
                 if (gS_all) {  // coalesced: a warp writes 8 whole rows of S
                   float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024 + a * 32 + 8 * q);
@@ -968,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
       }
     }
   } else if (warp == kWarpMma) {  // ===== MMA issuer (whole warp, one elected lane issues) =====
-    int it = 0, j = 0;
+    int it = 0, j = 0, nflush = 0;
     const uint32_t base = smem_u32(smem);
     const uint32_t opS = base + kOffOps, opA = opS + 2 * kOpBytes, opAt = opS + 4 * kOpBytes;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
@@ -978,6 +1024,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
           TC_TRACE_MMA(0);
           mbar_wait(&br->split_full[bf], par3(it));
           if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
+          if (ps == 0 && c > 0 && c % kFlush == 0) mbar_wait(&br->acc_free, (nflush++) & 1);
           tc_fence_after();
           TC_TRACE_MMA(1);
           const uint32_t X = base + kOffRaw + st * kStage;
@@ -987,7 +1034,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             if (ps == 0) {
               // G += Q~^T dO (attention.cpp:405)
               const int rows = min(kRows, N - c * kRows);
-              issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c == 0);
+              issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c % kFlush == 0);
               // dQ~ (unscaled) = dO S^T (:410-411): A = dO hi/lo in TMEM, B row n = S row n
               issue_rowout_ts<false>(D, D + 32, opS, opS + kOpBytes);
             } else {
@@ -1137,6 +1184,13 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             mbar_wait(&br->mma_done[bf], par3(it));
             tc_fence_after();
             TC_TRACE(3);
+            uint8_t* run = ops + 2 * kOpBytes;  // the dA operands' area, free until the G-epilogue
+            if (ps == 0 && c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush G
+              flush_acc(tmem, run, wq, lane, c == kFlush - 1);
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&br->acc_free);
+            }
             if (ps == 0) {
               // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428)
               float gq[32], xq[32];
@@ -1150,7 +1204,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               if (c == C - 1) {
                 // G complete: dm (:408), dA = s G (:412-413) as both state operands
                 float g8[8], h8[8], l8[8];
-                reduce_rows8(tmem, Y + kTile, wq, lane, g, t, g8);
+                reduce_rows8(tmem, Y + kTile, wq, lane, g, t, g8, C > kFlush ? run : nullptr);
                 const int a = t >> 2, q = t & 3;
                 double dot = 0.0;
 #pragma unroll

@@ -6,7 +6,7 @@ sys.path.insert(0, "tests")
 from test_gpu_parity import run_gpu, oracle_for, normwise  # noqa: E402
 from paper_2602_06935_b200 import _lib, inputs  # noqa: E402
 
-for N in (1, 2, 50, 65, 128, 200, 256, 513, 2048):
+for N in (1, 2, 50, 65, 128, 200, 256, 513, 2048, 4096, 16384):
     B, H, D = 8, 2, 32
     h = inputs.make_host(B, H, N, D, seed=N)
     valid = inputs.left_padded_mask(B, N, N)
