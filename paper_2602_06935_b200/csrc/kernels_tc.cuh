@@ -380,6 +380,19 @@ __device__ __forceinline__ void split32(const float (&x)[32], float (&h)[32], fl
     l[k + 1] = __uint_as_float(__float_as_uint(lv.y) & mask);
   }
 }
+// lo = x - trunc_tf32(x) only: tcgen05 kind::tf32 truncates fp32 operands
+// (measured, scripts/dev/tf32_round.cu), so an untouched fp32 tile already is
+// its own hi part and only lo has to be written.
+__device__ __forceinline__ void lo32(const float (&x)[32], float (&l)[32]) {
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const float h0 = __uint_as_float(__float_as_uint(x[k]) & 0xFFFFE000u);
+    const float h1 = __uint_as_float(__float_as_uint(x[k + 1]) & 0xFFFFE000u);
+    const float2 lv = __ffma2_rn(f2p(h0, h1), f2p(-1.f, -1.f), f2p(x[k], x[k + 1]));
+    l[k] = lv.x;
+    l[k + 1] = lv.y;
+  }
+}
 // Rows of a 32-byte-granule tile in "lane order": x[8q..8q+3] is the half of
 // granule q the lane touches first (see load_row32), x[8q+4..8q+7] the other.
 // Element-wise work (norms, scaling, hi/lo split) does not care about the order,
@@ -404,28 +417,6 @@ __device__ __forceinline__ void store_row32_raw(uint8_t* tile, int row, const fl
     *reinterpret_cast<float4*>(g + (sw ^ 16u)) =
         make_float4(x[8 * q + 4], x[8 * q + 5], x[8 * q + 6], x[8 * q + 7]);
   }
-}
-// Natural column order, no selects, 2-way bank conflicts (rows r and r+4 of a
-// warp share granule positions).  COTTEN_TC_P1_NATURAL picks this for the
-// backward's pass-1 tiles, whose rows are needed in natural order anyway.
-#ifndef COTTEN_TC_P1_NATURAL
-#define COTTEN_TC_P1_NATURAL 0
-#endif
-__device__ __forceinline__ void load_row32_nat(const uint8_t* tile, int row, float (&x)[32]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float4 v = *reinterpret_cast<const float4*>(tile + chunk_off32(row, j));
-    x[4 * j] = v.x;
-    x[4 * j + 1] = v.y;
-    x[4 * j + 2] = v.z;
-    x[4 * j + 3] = v.w;
-  }
-}
-__device__ __forceinline__ void store_row32_nat(uint8_t* tile, int row, const float (&x)[32]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    *reinterpret_cast<float4*>(tile + chunk_off32(row, j)) =
-        make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
 }
 // lane order -> natural column order (and back: the map is an involution)
 __device__ __forceinline__ void unswap32(float (&x)[32], int row) {
@@ -907,8 +898,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
               split32(kx, hh, ll, f ? 0xFFFFFFFFu : 0u);  // padded rows: exact zeros, NaN-safe
               store_row32_raw(X, t, hh);
               store_row32_raw(Y, t, ll);
-              split32(vx, hh, ll);
-              store_row32_raw(X + kTile, t, hh);
+              lo32(vx, ll);  // V: the TMA tile itself is the hi operand
               store_row32_raw(Y + kTile, t, ll);
             } else {  // Q~ for every row (attention.cpp:366-377), TMEM A operand of O = Q~ S
               float qx[32];
@@ -1115,37 +1105,23 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               // Q~ every row (:366-377, used again in :421-428); rows past N are exact
               // zeros in G even for eps = 0.  Tiles use the 32-byte-granule swizzle.
               float xr[32], hh[32], ll[32];
-#if COTTEN_TC_P1_NATURAL
-              load_row32_nat(X, t, xr);
-#else
               load_row32_raw(X, t, xr);
-#endif
               const float inv = rsqrtf(sumsq(xr) + eps);
               scale32(xr, r < N ? inv : 0.f);
               split32(xr, hh, ll);
-#if COTTEN_TC_P1_NATURAL
-              store_row32_nat(X, t, hh);
-              store_row32_nat(Y, t, ll);
-#else
+              TC_TRACE(3);
               store_row32_raw(X, t, hh);
               store_row32_raw(Y, t, ll);
               unswap32(xr, t);  // natural order: the dQ Jacobian pairs it with TMEM columns
-#endif
               tmem_st32(D + 96, xr);  // q~ and inv for the epiloguer's dQ Jacobian
               tmem_st1(tinv, inv);
-#if COTTEN_TC_P1_NATURAL
-              load_row32_nat(X + kTile, t, xr);  // dO
-              split32(xr, hh, ll);
-              store_row32_nat(X + kTile, t, hh);
-              store_row32_nat(Y + kTile, t, ll);
-#else
-              load_row32_raw(X + kTile, t, xr);  // dO
-              split32(xr, hh, ll);
-              store_row32_raw(X + kTile, t, hh);
+              TC_TRACE(4);
+              load_row32_raw(X + kTile, t, hh);  // dO: the TMA tile itself is the hi operand
+              lo32(hh, ll);
               store_row32_raw(Y + kTile, t, ll);
               unswap32(hh, t);
               unswap32(ll, t);
-#endif
+              TC_TRACE(5);
               tmem_st32(D + 32, hh);  // dO as the TMEM A operand of dQ~ = dO S^T
               tmem_st32(D + 64, ll);
               if (c == 0) {  // S rows (row n = S row n) for dQ~ = dO S^T
@@ -1171,8 +1147,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               scale32(kx, inv);  // padded rows may hold anything: masked, never multiplied in
               tmem_store_split(D + 64, kx, f ? 0xFFFFFFFFu : 0u);
               tmem_st1(tinv, inv);
-              load_row(X + kTile, t, kx);  // V
-              store_split(X + kTile, Y + kTile, t, kx);
+              load_row(X + kTile, t, kx);  // V: the TMA tile itself is the hi operand
+              float vl[32];
+              lo32(kx, vl);
+              store_row(Y + kTile, t, vl);
             }
             tmem_wait_st();
             tc_fence_before();

@@ -25,6 +25,13 @@ for tag in ("fwd", "bwd"):
     stat("epiloguer: staged arrive", (ep[..., 4] - ep[..., 5])[ok])
     stat("epiloguer: idle before next done", (ep[:, 1:, 3] - ep[:, :-1, 4])[okn])
     stat("epiloguer: period", (ep[:, 1:, 3] - ep[:, :-1, 3])[okn])
+    if tag == "bwd":
+        for kind in (0, 1):
+            sel = [it for it in range(K) if it % 4 == kind]
+            g = lambda x: np.concatenate([x[:, it][ok[:, it]] for it in sel]).mean()  # noqa: E731
+            print(f"  bwd p1 kind {kind} split phases: load+norm+split {g(sp[..., 3] - sp[..., 1]):5.0f}"
+                  f"  Q stores+unswap+tmem {g(sp[..., 4] - sp[..., 3]):5.0f}  dO load/split/stores+unswap {g(sp[..., 5] - sp[..., 4]):5.0f}"
+                  f"  dO tmem+S-op+wait {g(sp[..., 6] - sp[..., 5]):5.0f}  fence+arrive {g(sp[..., 2] - sp[..., 6]):5.0f}")
     for kind in range(4):
         sel = [it for it in range(K) if it % 4 == kind]
         f = lambda x: np.concatenate([x[:, it][ok[:, it]] for it in sel]).mean()  # noqa: E731

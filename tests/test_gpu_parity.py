@@ -145,7 +145,7 @@ def test_ml1m_unit_shape_f32(flags, mask_kind):
 
 
 @pytest.mark.parametrize("flags", PATHS[:2], ids=PATH_IDS[:2])
-@pytest.mark.parametrize("N", [1, 2, 7, 8, 9, 31, 32, 33, 50, 127, 128, 129, 200, 255, 256, 257,
+@pytest.mark.parametrize("N", [1, 2, 7, 8, 9, 31, 32, 33, 50, 65, 72, 96, 100, 127, 128, 129, 200, 255, 256, 257,
                                513, 1000, 2048, 4096, 16384])
 def test_seq_len_edges_f32(N, flags):
     B, H, D = (5, 2, 32) if N <= 2048 else (2, 2, 32)
