@@ -24,6 +24,8 @@ struct OpParams {
   double* dm_unit;       // [B*H] or nullptr
   int* status;           // sticky per-device status word (COTTEN_STATUS_*)
   void* workspace;       // kernel-specific global scratch (generic bwd: G per unit)
+  double* dm_total;      // tcgen05 bwd: fixed-order sum of dm_unit, written by the last CTA
+  unsigned* grid_done;   // tcgen05 bwd: zeroed CTA-completion counter (dm_total)
   int64_t B, H, N, D;
   int64_t sb, sh, sn, msb;
   double m, eps;

@@ -157,7 +157,7 @@ struct Scratch {
   void* ptr = nullptr;
   size_t bytes = 0;
   int dev = -1;
-  void* get(size_t need) {
+  void* get(size_t need, bool zeroed = false) {
     int cur = 0;
     COTTEN_CUDA(cudaGetDevice(&cur));
     if (dev != cur) {  // another device: drop our (stale) handle, allocate anew
@@ -169,12 +169,16 @@ struct Scratch {
       if (ptr) cudaFree(ptr);
       ptr = nullptr;
       COTTEN_CUDA(cudaMalloc(&ptr, need));
+      if (zeroed) COTTEN_CUDA(cudaMemset(ptr, 0, need));  // kernels keep it zero between launches
       bytes = need;
     }
     return ptr;
   }
 };
-thread_local Scratch g_dm_scratch, g_s_scratch, g_g_scratch;
+// g_counter: the CTA-completion counter of the tcgen05 backward's in-kernel dm
+// total (per host thread, like the other scratch: calls of one thread are
+// stream-ordered by the reference's usage).
+thread_local Scratch g_dm_scratch, g_s_scratch, g_g_scratch, g_counter;
 
 // ---- launches -------------------------------------------------------------
 
@@ -292,8 +296,15 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
   p.dv = dv;
   p.dm_unit = dm_unit;
   if (dm_total && !dm_unit) p.dm_unit = static_cast<double*>(g_dm_scratch.get(L.units() * sizeof(double)));
+  const bool tc_path = L.dtype == COTTEN_F32 &&
+                       !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE)) &&
+                       tc_bwd_supported<float>(p);
+  if (dm_total && tc_path) {  // the tcgen05 kernel's last CTA writes the total (no extra launch)
+    p.dm_total = dm_total;
+    p.grid_done = static_cast<unsigned*>(g_counter.get(sizeof(unsigned), true));
+  }
   launch_bwd(L, p, st);
-  if (dm_total) {
+  if (dm_total && !tc_path) {
     dm_reduce_kernel<<<1, 256, 0, st>>>(p.dm_unit, L.units(), dm_total);
     g_launches += 1;
     COTTEN_CUDA(cudaGetLastError());

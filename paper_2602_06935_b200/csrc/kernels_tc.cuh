@@ -45,6 +45,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -573,7 +574,21 @@ constexpr int kTraceItems = 64;
       static_cast<long long*>(p.workspace)[((blockIdx.x * 3 + 2) * kTraceItems + it) * 8 + (k)] = \
           clock64();                                                                      \
   } while (0)
+// CTA timeline in globaltimer ns (comparable across SMs): slot [cta][2][kTraceItems-1][k],
+// k = 4 kernel entry, 5 setup done, 6 last item finished (epiloguer), 7 CTA exit.
+#define TC_TRACE_CTA(k)                                                                   \
+  do {                                                                                    \
+    if (p.workspace) {                                                                    \
+      unsigned long long gt_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                              \
+      static_cast<long long*>(p.workspace)[((blockIdx.x * 3 + 2) * kTraceItems + kTraceItems - 1) * 8 + (k)] = \
+          (long long)gt_;                                                                 \
+    }                                                                                     \
+  } while (0)
 #else
+#define TC_TRACE_CTA(k) \
+  do {                  \
+  } while (0)
 #define TC_TRACE(k) \
   do {              \
   } while (0)
@@ -628,6 +643,43 @@ __device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* 
   __syncthreads();
   tc_fence_after();
   return *tslot;
+}
+// dm_total = fixed-order sum of dm_unit[0, units): the same partition and
+// tree as dm_reduce_kernel (kernels_generic.cuh), run by the last CTA to
+// finish, so the value is bit-identical to the separate launch it replaces.
+__device__ __forceinline__ void last_cta_dm_total(const OpParams& p, int units, uint8_t* smem_word) {
+  volatile unsigned* flag = reinterpret_cast<volatile unsigned*>(smem_word);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(p.grid_done, 1u);
+    *flag = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!*flag) return;
+  __threadfence();
+  double* red = reinterpret_cast<double*>(smem_word + 8);
+  if (threadIdx.x < 256) {
+    double part = 0.0;
+    const int64_t per = (units + 255) / 256;
+    const int64_t lo = threadIdx.x * per, hi = min64(units, lo + per);
+    for (int64_t u = lo; u < hi; ++u) part += __ldcg(p.dm_unit + u);  // contiguous, in order
+    part = warp_sum(part);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    *p.dm_total = t;
+    *p.grid_done = 0u;  // ready for the next launch
+  }
+}
+// Programmatic dependent launch: the setup above (barrier init, TMEM
+// allocation) runs while the previous kernel in the stream drains; every role
+// waits for that kernel's memory before its first global access.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void tc_teardown(uint32_t tmem, int warp) {
   tc_fence_before();
@@ -780,7 +832,11 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
   Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
   UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
   uint8_t* ops = smem + kOffOps;
+  if (threadIdx.x == 0) TC_TRACE_CTA(4);
   const uint32_t tmem = tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) TC_TRACE_CTA(5);
 
   if (warp == kWarpProducer) {  // ===== TMA: (K, V) chunks then Q chunks =====
     if (lane == 0) {
@@ -961,7 +1017,9 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
       if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
     }
   }
+  if (threadIdx.x == 128) TC_TRACE_CTA(6);  // epiloguer thread 0: its last item is done
   tc_teardown(tmem, warp);
+  if (threadIdx.x == 0) TC_TRACE_CTA(7);
 }
 
 // ======================================================================================
@@ -981,7 +1039,11 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
   UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
   double* dm_x = reinterpret_cast<double*>(smem + kOffMisc + 40);
   uint8_t* ops = smem + kOffOps;
+  if (threadIdx.x == 0) TC_TRACE_CTA(4);
   const uint32_t tmem = tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) TC_TRACE_CTA(5);
 
   if (warp == kWarpProducer) {  // ===== TMA: (Q, dO) chunks, then (K, V) chunks =====
     if (lane == 0) {
@@ -1266,7 +1328,13 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
       if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
     }
   }
+  if (threadIdx.x == 128) {
+    TC_TRACE_CTA(6);  // epiloguer thread 0: its last item is done
+    if (p.dm_total) __threadfence();  // this thread wrote the CTA's dm_unit entries
+  }
   tc_teardown(tmem, warp);
+  if (p.dm_total) last_cta_dm_total(p, units, smem + kOffRaw);
+  if (threadIdx.x == 0) TC_TRACE_CTA(7);
 }
 
 }  // namespace tc
@@ -1353,6 +1421,23 @@ inline void tc_trace_end(void* buf, int grid, const char* tag, cudaStream_t st) 
 #endif
 }
 
+// One CTA per SM, programmatic stream serialization (PDL) enabled.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tc::kThreads);
+  cfg.dynamicSmemBytes = tc::kSmemBytes;
+  cfg.stream = st;
+  static const bool pdl = getenv("COTTEN_NO_PDL") == nullptr;  // A/B switch
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 inline int launch_tc_fwd(const OpParams& p, cudaStream_t st) {
   CUtensorMap mq, mk, mv, mo;
   if (!make_chunk_map(&mq, p.q, p) || !make_chunk_map(&mk, p.k, p, true) ||
@@ -1365,7 +1450,7 @@ inline int launch_tc_fwd(const OpParams& p, cudaStream_t st) {
   const int grid = std::min(units, sm_count());
   OpParams q = p;
   q.workspace = tc_trace_begin(grid);
-  tc::cos_fwd_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(mq, mk, mv, mo, q);
+  if (launch_pdl(tc::cos_fwd_tc_kernel, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
   tc_trace_end(q.workspace, grid, "fwd", st);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
@@ -1384,8 +1469,8 @@ inline int launch_tc_bwd(const OpParams& p, cudaStream_t st) {
   const int grid = std::min(units, sm_count());
   OpParams q = p;
   q.workspace = tc_trace_begin(grid);
-  tc::cos_bwd_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, st>>>(mq, mk, mv, mg, mdq, mdk,
-                                                                     mdv, q);
+  if (launch_pdl(tc::cos_bwd_tc_kernel, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, q) != cudaSuccess)
+    return -1;
   tc_trace_end(q.workspace, grid, "bwd", st);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

@@ -37,3 +37,16 @@ for tag in ("fwd", "bwd"):
         f = lambda x: np.concatenate([x[:, it][ok[:, it]] for it in sel]).mean()  # noqa: E731
         print(f"  kind {kind} (it%4): split {f(sp[..., 2] - sp[..., 1]):6.0f}  mma {f(mm[..., 2] - mm[..., 1]):6.0f}"
               f"  epi {f(ep[..., 5] - ep[..., 3]):6.0f}  epi-staged {f(ep[..., 4] - ep[..., 5]):6.0f}")
+
+# CTA timelines (globaltimer ns): entry, setup done, last item done, exit
+for tag in ("fwd", "bwd"):
+    try:
+        a = np.fromfile(f"{sys.argv[1]}/{tag}.bin", dtype=np.int64).reshape(-1, 3, K, 8)
+    except FileNotFoundError:
+        continue
+    c = a[:, 2, K - 1, 4:8].astype(np.float64)
+    c = c[c[:, 0] > 0]
+    t0 = c[:, 0].min()
+    c = (c - t0) / 1e3  # us
+    print(f"{tag} CTA timeline (us from the first CTA entry): entry max {c[:, 0].max():.2f}  setup done mean {c[:, 1].mean():.2f}"
+          f"  last item done mean {c[:, 2].mean():.2f} max {c[:, 2].max():.2f}  exit max {c[:, 3].max():.2f}")
