@@ -48,6 +48,19 @@ WORKLOADS = {
     "ml20m": (65536, 200, 2, 32, 1, True,
               "BASELINE config #4: cosine-attn fwd+bwd, ML-20M shape (B=65536 split across GPUs, "
               "N=200, H=2, d_h=32), fp32, left-padded mask"),
+    # BASELINE config #5 (long-sequence sweep) points; ~0.5-1 G rows of work each
+    "long4k": (1024, 4096, 2, 32, 1, True,
+               "BASELINE config #5 point: cosine-attn fwd+bwd, N=4096, H=2, d_h=32, B=1024, fp32, "
+               "left-padded mask"),
+    "long16k": (256, 16384, 2, 32, 1, True,
+                "BASELINE config #5 point: cosine-attn fwd+bwd, N=16384, H=2, d_h=32, B=256, fp32, "
+                "left-padded mask"),
+    "long4k_d64": (512, 4096, 1, 64, 1, True,
+                   "BASELINE config #5 point: cosine-attn fwd+bwd, N=4096, H=1, d_h=64, B=512, fp32 "
+                   "(generic kernels), left-padded mask"),
+    "long4k_d128": (256, 4096, 1, 128, 1, True,
+                    "BASELINE config #5 point: cosine-attn fwd+bwd, N=4096, H=1, d_h=128, B=256, fp32 "
+                    "(generic kernels), left-padded mask"),
 }
 L2_FLUSH_BYTES = 256 << 20
 

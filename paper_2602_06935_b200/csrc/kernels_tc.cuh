@@ -1361,7 +1361,10 @@ inline bool make_chunk_map(CUtensorMap* map, const void* base, const OpParams& p
 
 // Sequences of <= 64 rows would leave half of every 128-row chunk empty; the
 // FP32-pipe kernels (kernels_d32.cuh) serve them until units are packed.
-constexpr int64_t kTcMinN = 65;
+#ifndef COTTEN_TC_MIN_N
+#define COTTEN_TC_MIN_N 65
+#endif
+constexpr int64_t kTcMinN = COTTEN_TC_MIN_N;
 
 inline bool tc_layout_ok(const OpParams& p, std::initializer_list<const void*> ptrs) {
   if (p.D != 32 || p.N < kTcMinN || p.N > tc::kMaxN) return false;
