@@ -605,6 +605,7 @@ struct Bars {
   uint64_t split_full[kRing], mma_done[kRing];  // splitter -> MMA -> epiloguer
   uint64_t op_ready;                    // state operand (S or dA) written, per unit
   uint64_t acc_free;                    // epiloguer flushed the reduction accumulator
+  uint64_t red_done;                    // bwd: a unit's G reduction MMAs complete (per unit)
   uint64_t fl_full[2], fl_empty[2];     // mask warp <-> workers (slot = unit & 1)
   uint64_t staged[kRing], lo_free[kRing];  // epiloguer -> store warp -> splitter
 };
@@ -632,6 +633,7 @@ __device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* 
     }
     mbar_init(&br->op_ready, 1);
     mbar_init(&br->acc_free, 4);
+    mbar_init(&br->red_done, 1);
     d32::fence_barrier_init();
   }
   if (warp == kWarpMma) {
@@ -1087,6 +1089,9 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               // G += Q~^T dO (attention.cpp:405)
               const int rows = min(kRows, N - c * kRows);
               issue_reduction(tmem, X, X + kTile, Y - X, (rows + 7) >> 3, c % kFlush == 0);
+              // G is complete: the epiloguer starts the G-epilogue (the path to the
+              // pass-2 MMAs) while the dQ~ MMAs below still run
+              if (c == C - 1) mma_commit(&br->red_done);
               // dQ~ (unscaled) = dO S^T (:410-411): A = dO hi/lo in TMEM, B row n = S row n
               issue_rowout_ts<false>(D, D + 32, opS, opS + kOpBytes);
             } else {
@@ -1221,10 +1226,50 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             if (lane == 0) mbar_arrive(&br->split_full[bf]);
             TC_TRACE(2);
           } else {  // ---------------- epiloguer ----------------
+            uint8_t* run = ops + 2 * kOpBytes;  // the dA operands' area, free until the G-epilogue
+            if (ps == 0 && c == C - 1) {
+              // G-epilogue first: it gates the pass-2 MMAs, the dQ epilogue does not
+              mbar_wait(&br->red_done, j & 1);
+              tc_fence_after();
+              // G complete: dm (:408), dA = s G (:412-413) as both state operands
+              float g8[8], h8[8], l8[8];
+              reduce_rows8(tmem, Y + kTile, wq, lane, g, t, g8, C > kFlush ? run : nullptr);
+              const int a = t >> 2, q = t & 3;
+              double dot = 0.0;
+#pragma unroll
+              for (int hh2 = 0; hh2 < 2; ++hh2) {  // <G, S> (S row a = K-major operand row a)
+                const float4 sh = *reinterpret_cast<const float4*>(ops + chunk_off(a, 2 * q + hh2));
+                const float4 sl4 =
+                    *reinterpret_cast<const float4*>(ops + kOpBytes + chunk_off(a, 2 * q + hh2));
+                float d = g8[4 * hh2] * (sh.x + sl4.x);
+                d = fmaf(g8[4 * hh2 + 1], sh.y + sl4.y, d);
+                d = fmaf(g8[4 * hh2 + 2], sh.z + sl4.z, d);
+                d = fmaf(g8[4 * hh2 + 3], sh.w + sl4.w, d);
+                dot += (double)d;
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k) g8[k] *= uc.s;  // dA row a, columns 8q..8q+7
+              split8(g8, h8, l8);
+              store8_k(ops + 2 * kOpBytes, a, q, h8);  // K-major B of dK~ = V dA^T
+              store8_k(ops + 3 * kOpBytes, a, q, l8);
+              store8_mn(ops + 4 * kOpBytes, a, q, h8);  // MN-major B of dV = K~ dA
+              store8_mn(ops + 5 * kOpBytes, a, q, l8);
+              // fixed-order dm: warp tree, then the 4 warps of the group in order
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+              if (lane == 0) dm_x[wq] = dot;
+              fence_proxy_async();
+              tc_fence_before();
+              group_sync(g);
+              if (t == 0) {  // dm partials read before op_ready lets the next G-epilogue run
+                const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
+                if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
+                mbar_arrive(&br->op_ready);
+              }
+            }
             mbar_wait(&br->mma_done[bf], par3(it));
             tc_fence_after();
             TC_TRACE(3);
-            uint8_t* run = ops + 2 * kOpBytes;  // the dA operands' area, free until the G-epilogue
             if (ps == 0 && c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush G
               flush_acc(tmem, run, wq, lane, c == kFlush - 1);
               tc_fence_before();
@@ -1241,45 +1286,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               scale32(gq, uc.s);
               jacobian32(gq, xq, dot32(gq, xq), inv);
               store_row(Y, t, gq);  // staged in the lo buffer (free: the MMAs are done)
-              if (c == C - 1) {
-                // G complete: dm (:408), dA = s G (:412-413) as both state operands
-                float g8[8], h8[8], l8[8];
-                reduce_rows8(tmem, Y + kTile, wq, lane, g, t, g8, C > kFlush ? run : nullptr);
-                const int a = t >> 2, q = t & 3;
-                double dot = 0.0;
-#pragma unroll
-                for (int hh2 = 0; hh2 < 2; ++hh2) {  // <G, S> (S row a = K-major operand row a)
-                  const float4 sh = *reinterpret_cast<const float4*>(ops + chunk_off(a, 2 * q + hh2));
-                  const float4 sl4 =
-                      *reinterpret_cast<const float4*>(ops + kOpBytes + chunk_off(a, 2 * q + hh2));
-                  float d = g8[4 * hh2] * (sh.x + sl4.x);
-                  d = fmaf(g8[4 * hh2 + 1], sh.y + sl4.y, d);
-                  d = fmaf(g8[4 * hh2 + 2], sh.z + sl4.z, d);
-                  d = fmaf(g8[4 * hh2 + 3], sh.w + sl4.w, d);
-                  dot += (double)d;
-                }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) g8[k] *= uc.s;  // dA row a, columns 8q..8q+7
-                split8(g8, h8, l8);
-                store8_k(ops + 2 * kOpBytes, a, q, h8);  // K-major B of dK~ = V dA^T
-                store8_k(ops + 3 * kOpBytes, a, q, l8);
-                store8_mn(ops + 4 * kOpBytes, a, q, h8);  // MN-major B of dV = K~ dA
-                store8_mn(ops + 5 * kOpBytes, a, q, l8);
-                // fixed-order dm: warp tree, then the 4 warps of the group in order
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                if (lane == 0) dm_x[wq] = dot;
-                fence_proxy_async();
-                tc_fence_before();
-                group_sync(g);
-                if (t == 0) {  // dm partials read before op_ready lets the next G-epilogue run
-                  const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
-                  if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
-                  mbar_arrive(&br->op_ready);
-                }
-              } else {
-                tc_fence_before();
-              }
+              tc_fence_before();
             } else {
               // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439); dK_i = v_i ? (g - (g.k~)k~)/nk : 0 (:430-437)
               const bool f = r < N && flag_at(fl, r);
