@@ -1192,6 +1192,9 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
               tmem_st32(D + 32, hh);  // dO as the TMEM A operand of dQ~ = dO S^T
               tmem_st32(D + 64, ll);
               if (c == 0) {  // S rows (row n = S row n) for dQ~ = dO S^T
+                // the previous unit's G-epilogue (dm) and dQ~ MMAs have read its S rows
+                // (op_ready follows both); matters for C == 1, already true for C >= 2
+                if (j > 0) mbar_wait(&br->op_ready, (j - 1) & 1);
 #pragma unroll
                 for (int e2 = 0; e2 < 2; ++e2) {
                   const int e = t + 128 * e2;
