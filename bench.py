@@ -57,10 +57,10 @@ WORKLOADS = {
                 "left-padded mask"),
     "long4k_d64": (512, 4096, 1, 64, 1, True,
                    "BASELINE config #5 point: cosine-attn fwd+bwd, N=4096, H=1, d_h=64, B=512, fp32 "
-                   "(generic kernels), left-padded mask"),
+                   "(register-tiled FP32-pipe kernels), left-padded mask"),
     "long4k_d128": (256, 4096, 1, 128, 1, True,
                     "BASELINE config #5 point: cosine-attn fwd+bwd, N=4096, H=1, d_h=128, B=256, fp32 "
-                    "(generic kernels), left-padded mask"),
+                    "(register-tiled FP32-pipe kernels), left-padded mask"),
 }
 L2_FLUSH_BYTES = 256 << 20
 
@@ -71,6 +71,25 @@ def algorithmic_bytes(B, H, N, D, elt=4):
     fwd = B * H * 4 * N * D * elt + B * N
     bwd = B * H * 7 * N * D * elt + B * N
     return fwd, bwd
+
+
+FP32_PEAK_FLOPS = 148 * 128 * 2 * 1.965e9
+
+
+def pipe_flops(B, H, N, D):
+    """SURVEY §8d flops per launch: fwd 4·N·d² + 7·N·d, bwd 8·N·d² + 12·N·d per unit."""
+    return B * H * (4 * N * D * D + 7 * N * D), B * H * (8 * N * D * D + 12 * N * D)
+
+
+def kernel_path(path, N, D):
+    """The kernels the library picks for this shape (cotten_capi.cu launch_*_t)."""
+    if D == 32 and path == "tcgen05" and N > 64:
+        return "tcgen05 (kernels_tc.cuh)"
+    if D == 32:
+        return "fp32pipe (kernels_d32.cuh)"
+    if D in (64, 128):
+        return "fp32-rt register-tiled FP32 pipe (kernels_rt.cuh)"
+    return "generic (kernels_generic.cuh)"
 
 
 def load_peaks():
@@ -361,7 +380,7 @@ def run_ours(args, world, rank, local):
         "config": {"workload": desc, "name": args.workload, "global_batch": global_b,
                    "batch_per_gpu": B, "seq_len": N, "heads": H, "head_dim": D, "model_dim": H * D,
                    "layers": layers, "parallelism": f"dp{world} (batch x head shards)",
-                   "kernel_path": args.path,
+                   "kernel_path": kernel_path(args.path, N, D),
                    "launch": "eager" if args.no_graph else ("one CUDA graph per op call, replayed back to back "
                                                               "(events at step boundaries); per-op kernel times "
                                                               "from a separately marked pass"),
@@ -377,6 +396,19 @@ def run_ours(args, world, rank, local):
         "gpu_launches": gpu_launches,
         "clocks": clocks,
     }
+    if D != 32:  # FP32-pipe kernels: compute at peak bounds them, not HBM (north star: max of both)
+        ff, fb = pipe_flops(B, H, N, D)
+        t_f = max(ff / FP32_PEAK_FLOPS, fwd_bytes / (peak * 1e9))
+        t_b = max(fb / FP32_PEAK_FLOPS, bwd_bytes / (peak * 1e9))
+        res["roofline_max"] = {
+            "model": "max(compute-at-peak, bytes-at-HBM) per launch; FP32 pipe peak = 148 SM x 128 FFMA "
+                     "x 2 x 1.965 GHz (derived, no measured FP32 peak in MEASURED_PEAKS.json)",
+            "pipe": "fp32", "peak_tflops": FP32_PEAK_FLOPS / 1e12,
+            "fwd_bound": "fp32" if ff / FP32_PEAK_FLOPS > fwd_bytes / (peak * 1e9) else "hbm",
+            "bwd_bound": "fp32" if fb / FP32_PEAK_FLOPS > bwd_bytes / (peak * 1e9) else "hbm",
+            "fwd_tflops": ff / fwd_avg / 1e12, "bwd_tflops": fb / bwd_avg / 1e12,
+            "fwd_frac": t_f / fwd_avg, "bwd_frac": t_b / bwd_avg,
+            "step_frac": layers * (t_f + t_b) / (ms_per_step / 1e3)}
     traffic = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic):
         try:

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -14,6 +15,7 @@
 #include "common.cuh"
 #include "kernels_d32.cuh"
 #include "kernels_generic.cuh"
+#include "kernels_rt.cuh"
 #include "kernels_tc.cuh"
 
 namespace cotten {
@@ -196,6 +198,9 @@ void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fast forward launch failed (tensor map)"};
     g_launches += n;
+  } else if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && rt_supported<T>(p, false)) {
+    if constexpr (!std::is_same<T, double>::value) launch_rt_fwd<T>(p, st);
+    g_launches += 1;
   } else {
     check_generic_fits(L);
     const size_t smem = gen_fwd_smem<A>(L.D);
@@ -221,6 +226,9 @@ void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fast backward launch failed (tensor map)"};
     g_launches += n;
+  } else if (!(L.flags & COTTEN_FLAG_FORCE_GENERIC) && rt_supported<T>(p, true)) {
+    if constexpr (!std::is_same<T, double>::value) launch_rt_bwd<T>(p, st);
+    g_launches += 1;
   } else {
     const bool gg = gen_bwd_smem<A>(L.D) > kSmemBudget;
     if (gen_bwd_smem<A>(L.D, gg) > kSmemBudget)

@@ -183,6 +183,68 @@ def test_bf16_within_stated_tolerance(D):
     assert_parity(res, oracle_for(res["inputs"], valid, 1.0, 1e-6), valid, "bf16")
 
 
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("N", [7, 33, 64, 65, 200, 513, 1000, 4096])
+def test_head_dim_64_128_seq_lens_f32(D, N):
+    """kernels_rt.cuh (register-tiled FP32 pipe): tile edges (TR = 64 / 32
+    rows), the 512-row running-sum flush, left-padded masks."""
+    B, H = (3, 2) if N <= 1000 else (2, 1)
+    h = inputs.make_host(B, H, N, D, seed=N + D)
+    valid = inputs.left_padded_mask(B, N, N)
+    res = run_gpu(h, valid, 0.75, 1e-6, "f32")
+    assert_parity(res, oracle_for(res["inputs"], valid, 0.75, 1e-6), valid, "f32")
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_head_dim_64_128_single_row(D):
+    """N = 1 reduces every output to one d_h-term dot product times a vector:
+    O and dV scale with q~.k~, dQ and dK with dO.v (S = k~ v^T, G = q~ dO^T).
+    Those dots cancel for some units, and an fp32 sum of d_h terms is accurate
+    to ~d_h u sum|terms|, not to 1e-5 of a cancelled result; each output's
+    error is therefore scaled by its dot's condition number sum|x_a y_a| /
+    |x.y| (the same kind of scaling the d_h <= 2 tests use)."""
+    B, H, N = 3, 2, 1
+    h = inputs.make_host(B, H, N, D, seed=N + D)
+    valid = inputs.left_padded_mask(B, N, N)
+    res = run_gpu(h, valid, 0.75, 1e-6, "f32")
+    out, dq, dk, dv, dm = oracle_for(res["inputs"], valid, 0.75, 1e-6)
+    x = {n: res["inputs"][n][:, :, 0, :].astype(np.float64) for n in ("q", "k", "v", "d_out")}
+    unit = lambda a: a / np.linalg.norm(a, axis=-1, keepdims=True)  # noqa: E731
+
+    def cond(a, b):
+        prod = a * b
+        return np.maximum((np.abs(prod).sum(-1) / np.abs(prod.sum(-1))).reshape(-1), 1.0)
+
+    c_qk, c_dov = cond(unit(x["q"]), unit(x["k"])), cond(x["d_out"], x["v"])
+    for name, want, c in (("out", out, c_qk), ("dv", dv, c_qk), ("dq", dq, c_dov), ("dk", dk, c_dov)):
+        g = res[name].reshape(B * H, -1).astype(np.float64)
+        w = want.reshape(B * H, -1)
+        err = np.abs(g - w).max(1) / np.abs(w).max(1)
+        assert np.all(err / c <= 1e-5), (name, err, c)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_head_dim_128_random_mask(dtype):
+    B, H, N, D = 4, 2, 300, 128
+    h = inputs.make_host(B, H, N, D, seed=21)
+    valid = inputs.random_mask(B, N, 21)
+    res = run_gpu(h, valid, 1.0, 1e-6, dtype)
+    assert_parity(res, oracle_for(res["inputs"], valid, 1.0, 1e-6), valid, dtype)
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_nan_in_padded_key_rows_never_read_rt(D):
+    B, H, N = 3, 2, 150
+    h = inputs.make_host(B, H, N, D, seed=22)
+    valid = inputs.left_padded_mask(B, N, 22)
+    clean = run_gpu(h, valid, 1.0, 1e-6)
+    h2 = {n: x.copy() for n, x in h.items()}
+    h2["k"][np.broadcast_to((valid == 0)[:, None, :], (B, H, N))] = np.nan
+    dirty = run_gpu(h2, valid, 1.0, 1e-6)
+    for n in ("out", "dq", "dk", "dv"):
+        np.testing.assert_array_equal(clean[n], dirty[n])
+
+
 def test_bnhd_strided_layout_equals_contiguous():
     B, H, N, D = 6, 2, 200, 32
     h = inputs.make_host(B, H, N, D, seed=5)
