@@ -10,7 +10,8 @@
 //             phase B: dK~ = V dA^T, dV = K~ dA, dK Jacobian, masks (:415-416, :430-439)
 //
 // Rows stream through shared memory in tiles of TR rows (64 for d_h = 64,
-// 32 for 128), loaded with 16-byte (f32) / 8-byte (bf16) coalesced loads;
+// 32 for 128), double-buffered: tile i+1 is fetched into registers with
+// 16-byte (f32) / 8-byte (bf16) coalesced loads while tile i is computed;
 // the row norm is a shuffle reduction over the 16 / 32 threads that load
 // the row, and normalisation / masking happen on the way into shared memory.
 //   * reductions (S, G): thread (ab, cb) owns a (d/16) x (d/16) block of the
@@ -49,8 +50,13 @@ struct Cfg {
   static constexpr int F4 = D / 4;              // 4-element groups per row
   static constexpr int LD = TR * F4 / kThreads; // 4-element loads per thread per tile
   static constexpr int kFlushTiles = 512 / TR;  // running-sum flush period (512 rows)
-  static constexpr size_t fwd_smem = sizeof(float) * (2 * TR * D + D * D + TR);
-  static constexpr size_t bwd_smem = sizeof(float) * (2 * TR * D + 2 * D * D + TR) + 8 * sizeof(double);
+  // tile row stride: +16 B so rows rb and rb + 1 (read together by a warp in
+  // the row outputs) fall in different banks
+  static constexpr int LDT = D + 4;
+  // two tile buffers (double-buffered: tile i+1's loads are in flight while
+  // tile i is computed) of two tensors each, the state(s), 1/norm per buffer
+  static constexpr size_t fwd_smem = sizeof(float) * (4 * TR * LDT + D * D + 2 * TR);
+  static constexpr size_t bwd_smem = sizeof(float) * (4 * TR * LDT + 2 * D * D + 2 * TR) + 8 * sizeof(double);
 };
 
 __device__ __forceinline__ float4 ld4(const float* p) {
@@ -75,23 +81,35 @@ __device__ __forceinline__ void st4(__nv_bfloat16* p, float a, float b, float c,
 
 enum TileMode { kRaw, kQuery, kKey };
 
-// Rows [t0, t0 + TR) of X into sm[TR][D] (rows >= N are zeros).  kQuery:
-// every row < N scaled by 1/sqrt(|x|^2 + eps) (:366-377); kKey: valid rows
-// scaled, padded rows exact zeros by select (:334-342).  rinv[r] = the factor;
-// norm_out (optional): sqrt(|x|^2 + eps), 1.0 for padded keys (:336, :343).
+// Rows [t0, t0 + TR) of X into registers (rows >= N are zeros); thread
+// tid holds 4-element groups f = tid + 256 k (row f / F4, group f % F4).
 template <typename T, int D>
-__device__ __forceinline__ void load_tile(float* sm, float* rinv, const T* X, int64_t base,
-                                          int64_t sn, int64_t N, int64_t t0, TileMode mode,
-                                          const uint8_t* vrow, float eps, float* norm_out) {
+__device__ __forceinline__ void fetch_tile(float4 (&reg)[Cfg<D>::LD], const T* X, int64_t base,
+                                           int64_t sn, int64_t N, int64_t t0) {
   using C = Cfg<D>;
-  const int tid = threadIdx.x;
 #pragma unroll
   for (int k = 0; k < C::LD; ++k) {
-    const int f = tid + kThreads * k;
+    const int f = threadIdx.x + kThreads * k;
+    const int64_t row = t0 + f / C::F4;
+    reg[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < N) reg[k] = ld4(X + base + row * sn + 4 * (f % C::F4));
+  }
+}
+// The fetched rows into sm[TR][D].  kQuery: every row < N scaled by
+// 1/sqrt(|x|^2 + eps) (:366-377); kKey: valid rows scaled, padded rows exact
+// zeros by select (:334-342).  rinv[r] = the factor; norm_out (optional):
+// sqrt(|x|^2 + eps), 1.0 for padded keys (:336, :343).
+template <int D>
+__device__ __forceinline__ void put_tile(float* sm, float* rinv, const float4 (&reg)[Cfg<D>::LD],
+                                         int64_t N, int64_t t0, TileMode mode, const uint8_t* vrow,
+                                         float eps, float* norm_out) {
+  using C = Cfg<D>;
+#pragma unroll
+  for (int k = 0; k < C::LD; ++k) {
+    const int f = threadIdx.x + kThreads * k;
     const int r = f / C::F4, c4 = f % C::F4;
     const int64_t row = t0 + r;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (row < N) v = ld4(X + base + row * sn + 4 * c4);
+    float4 v = reg[k];
     if (mode != kRaw) {
       float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
 #pragma unroll
@@ -106,7 +124,7 @@ __device__ __forceinline__ void load_tile(float* sm, float* rinv, const T* X, in
         if (norm_out && row < N) norm_out[row] = keep ? nrm : 1.0f;
       }
     }
-    *reinterpret_cast<float4*>(sm + r * D + 4 * c4) = v;
+    *reinterpret_cast<float4*>(sm + r * C::LDT + 4 * c4) = v;
   }
 }
 
@@ -120,12 +138,12 @@ __device__ __forceinline__ void reduce_tile(float (&acc)[Cfg<D>::RA][Cfg<D>::RC]
     float xa[C::RA], yc[C::RC];
 #pragma unroll
     for (int g = 0; g < C::RA / 4; ++g) {
-      const float4 u = *reinterpret_cast<const float4*>(x + r * D + 64 * g + 4 * ab);
+      const float4 u = *reinterpret_cast<const float4*>(x + r * C::LDT + 64 * g + 4 * ab);
       xa[4 * g] = u.x; xa[4 * g + 1] = u.y; xa[4 * g + 2] = u.z; xa[4 * g + 3] = u.w;
     }
 #pragma unroll
     for (int g = 0; g < C::RC / 4; ++g) {
-      const float4 u = *reinterpret_cast<const float4*>(y + r * D + 64 * g + 4 * cb);
+      const float4 u = *reinterpret_cast<const float4*>(y + r * C::LDT + 64 * g + 4 * cb);
       yc[4 * g] = u.x; yc[4 * g + 1] = u.y; yc[4 * g + 2] = u.z; yc[4 * g + 3] = u.w;
     }
 #pragma unroll
@@ -173,7 +191,7 @@ __device__ __forceinline__ void rowout_tile(float (&out)[Cfg<D>::RR][Cfg<D>::RC]
   for (int x = 0; x < D; x += 4) {
     float4 xr[C::RR];
 #pragma unroll
-    for (int k = 0; k < C::RR; ++k) xr[k] = *reinterpret_cast<const float4*>(X + (rb + 16 * k) * D + x);
+    for (int k = 0; k < C::RR; ++k) xr[k] = *reinterpret_cast<const float4*>(X + (rb + 16 * k) * C::LDT + x);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float m[C::RC];
@@ -227,10 +245,10 @@ template <typename T, int D>
 __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
   using C = Cfg<D>;
   extern __shared__ __align__(16) float sm[];
-  float* X0 = sm;
-  float* X1 = X0 + C::TR * D;
-  float* Ssm = X1 + C::TR * D;  // running S, then the B operand of O = Q~ S
-  float* rinv = Ssm + D * D;
+  constexpr int TD = C::TR * C::LDT;
+  float* tiles = sm;              // [buffer][tensor][TR][D]
+  float* Ssm = tiles + 4 * TD;    // running S, then the B operand of O = Q~ S
+  float* rinv_all = Ssm + D * D;  // [buffer][TR]
   __shared__ int s_cnt;
   const int64_t unit = blockIdx.x, N = p.N;
   const int64_t b = unit / p.H, h = unit - b * p.H;
@@ -253,16 +271,28 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
   for (int i = 0; i < C::RA; ++i)
 #pragma unroll
     for (int j = 0; j < C::RC; ++j) acc[i][j] = 0.f;
+  const T* K = static_cast<const T*>(p.k);
+  const T* V = static_cast<const T*>(p.v);
+  const T* Q = static_cast<const T*>(p.q);
+  float4 ra[C::LD], rb4[C::LD];
+  fetch_tile<T, D>(ra, K, base, p.sn, N, 0);
+  fetch_tile<T, D>(rb4, V, base, p.sn, N, 0);
   int nt = 0;
   for (int64_t t0 = 0; t0 < N; t0 += C::TR, ++nt) {
-    load_tile<T, D>(X0, rinv, static_cast<const T*>(p.k), base, p.sn, N, t0, kKey, vrow, eps,
-                    norms ? norms + N : nullptr);
-    load_tile<T, D>(X1, rinv, static_cast<const T*>(p.v), base, p.sn, N, t0, kRaw, vrow, eps, nullptr);
-    __syncthreads();
+    float* X0 = tiles + (nt & 1) * 2 * TD;
+    float* X1 = X0 + TD;
+    float* rinv = rinv_all + (nt & 1) * C::TR;
+    put_tile<D>(X0, rinv, ra, N, t0, kKey, vrow, eps, norms ? norms + N : nullptr);
+    put_tile<D>(X1, rinv, rb4, N, t0, kRaw, vrow, eps, nullptr);
+    __syncthreads();  // also: every thread is done with the tile this buffer held two steps ago
+    if (t0 + C::TR < N) {
+      fetch_tile<T, D>(ra, K, base, p.sn, N, t0 + C::TR);
+      fetch_tile<T, D>(rb4, V, base, p.sn, N, t0 + C::TR);
+    }
     reduce_tile<D>(acc, X0, X1, (int)min64(C::TR, N - t0), ab, cb);
     if ((nt + 1) % C::kFlushTiles == 0 || t0 + C::TR >= N) flush_state<D>(acc, Ssm, ab, cb);
-    __syncthreads();
   }
+  __syncthreads();
   if (p.saved_S) {
     float* dst = static_cast<float*>(p.saved_S) + unit * (int64_t)D * D;
     for (int e = tid; e < D * D / 4; e += kThreads)
@@ -272,9 +302,14 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
 
   T* O = static_cast<T*>(p.out);
   const int rb = tid >> 4;
-  for (int64_t t0 = 0; t0 < N; t0 += C::TR) {
-    load_tile<T, D>(X0, rinv, static_cast<const T*>(p.q), base, p.sn, N, t0, kQuery, nullptr, eps, norms);
+  fetch_tile<T, D>(ra, Q, base, p.sn, N, 0);
+  nt = 0;
+  for (int64_t t0 = 0; t0 < N; t0 += C::TR, ++nt) {
+    float* X0 = tiles + (nt & 1) * 2 * TD;
+    float* rinv = rinv_all + (nt & 1) * C::TR;
+    put_tile<D>(X0, rinv, ra, N, t0, kQuery, nullptr, eps, norms);
     __syncthreads();
+    if (t0 + C::TR < N) fetch_tile<T, D>(ra, Q, base, p.sn, N, t0 + C::TR);
     if (O) {
       float o[C::RR][C::RC];
       rowout_tile<D>(o, X0, Ssm, rb, cb);
@@ -286,7 +321,6 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
         if (row < N) store_row<T, D>(O + base + row * p.sn, o[k], cb);
       }
     }
-    __syncthreads();
   }
 }
 
@@ -294,12 +328,12 @@ template <typename T, int D>
 __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
   using C = Cfg<D>;
   extern __shared__ __align__(16) float sm[];
-  float* X0 = sm;                   // Q~ / K~ tile
-  float* X1 = X0 + C::TR * D;       // dO / V tile
-  float* Bt = X1 + C::TR * D;       // S^T (phase A), then dA^T (phase B)
+  constexpr int TD = C::TR * C::LDT;
+  float* tiles = sm;                // [buffer][Q~ or K~ | dO or V][TR][D]
+  float* Bt = tiles + 4 * TD;       // S^T (phase A), then dA^T (phase B)
   float* Bn = Bt + D * D;           // G running sum, then dA
-  float* rinv = Bn + D * D;
-  double* red = reinterpret_cast<double*>(rinv + C::TR + (C::TR & 1));
+  float* rinv_all = Bn + D * D;     // [buffer][TR]
+  double* red = reinterpret_cast<double*>(rinv_all + 2 * C::TR);
   __shared__ int s_cnt;
   const int64_t unit = blockIdx.x, N = p.N;
   const int64_t b = unit / p.H, h = unit - b * p.H;
@@ -335,12 +369,26 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
   for (int i = 0; i < C::RA; ++i)
 #pragma unroll
     for (int j = 0; j < C::RC; ++j) acc[i][j] = 0.f;
+  const T* Q = static_cast<const T*>(p.q);
+  const T* dO = static_cast<const T*>(p.dout);
+  const T* K = static_cast<const T*>(p.k);
+  const T* V = static_cast<const T*>(p.v);
+  float4 ra[C::LD], rb4[C::LD];
+  fetch_tile<T, D>(ra, Q, base, p.sn, N, 0);
+  fetch_tile<T, D>(rb4, dO, base, p.sn, N, 0);
   int nt = 0;
   // Phase A: G = Q~^T dO over all rows; dQ (all rows)
   for (int64_t t0 = 0; t0 < N; t0 += C::TR, ++nt) {
-    load_tile<T, D>(X0, rinv, static_cast<const T*>(p.q), base, p.sn, N, t0, kQuery, nullptr, eps, nullptr);
-    load_tile<T, D>(X1, rinv, static_cast<const T*>(p.dout), base, p.sn, N, t0, kRaw, nullptr, eps, nullptr);
+    float* X0 = tiles + (nt & 1) * 2 * TD;
+    float* X1 = X0 + TD;
+    float* rinv = rinv_all + (nt & 1) * C::TR;
+    put_tile<D>(X0, rinv, ra, N, t0, kQuery, nullptr, eps, nullptr);
+    put_tile<D>(X1, rinv, rb4, N, t0, kRaw, nullptr, eps, nullptr);
     __syncthreads();
+    if (t0 + C::TR < N) {
+      fetch_tile<T, D>(ra, Q, base, p.sn, N, t0 + C::TR);
+      fetch_tile<T, D>(rb4, dO, base, p.sn, N, t0 + C::TR);
+    }
     reduce_tile<D>(acc, X0, X1, (int)min64(C::TR, N - t0), ab, cb);
     if ((nt + 1) % C::kFlushTiles == 0 || t0 + C::TR >= N) flush_state<D>(acc, Bn, ab, cb);
     float o[C::RR][C::RC];
@@ -350,11 +398,11 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
       const int r = rb + 16 * k;
 #pragma unroll
       for (int j = 0; j < C::RC; ++j) o[k][j] *= scale;
-      const float d = row_dot<D>(o[k], X0 + r * D, cb);
+      const float d = row_dot<D>(o[k], X0 + r * C::LDT, cb);
       const float iv = rinv[r];
 #pragma unroll
       for (int g = 0; g < C::RC / 4; ++g) {
-        const float4 q = *reinterpret_cast<const float4*>(X0 + r * D + 64 * g + 4 * cb);
+        const float4 q = *reinterpret_cast<const float4*>(X0 + r * C::LDT + 64 * g + 4 * cb);
         o[k][4 * g] = (o[k][4 * g] - d * q.x) * iv;
         o[k][4 * g + 1] = (o[k][4 * g + 1] - d * q.y) * iv;
         o[k][4 * g + 2] = (o[k][4 * g + 2] - d * q.z) * iv;
@@ -362,8 +410,10 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
       }
       if (t0 + r < N) store_row<T, D>(dQ + base + (t0 + r) * p.sn, o[k], cb);
     }
-    __syncthreads();
   }
+  fetch_tile<T, D>(ra, K, base, p.sn, N, 0);  // phase B's first tile, in flight during dm / dA
+  fetch_tile<T, D>(rb4, V, base, p.sn, N, 0);
+  __syncthreads();
 
   // dm = -ln(n) s <G, S> (:408): fixed-order (thread, warp tree, warps in order)
   {
@@ -391,10 +441,18 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
   for (int e = tid; e < D * D; e += kThreads) Bn[e] *= scale;
 
   // Phase B: dK (valid rows), dV (valid rows); padded rows exact zeros (:430-439)
-  for (int64_t t0 = 0; t0 < N; t0 += C::TR) {
-    load_tile<T, D>(X0, rinv, static_cast<const T*>(p.k), base, p.sn, N, t0, kKey, vrow, eps, nullptr);
-    load_tile<T, D>(X1, rinv, static_cast<const T*>(p.v), base, p.sn, N, t0, kRaw, vrow, eps, nullptr);
+  nt = 0;
+  for (int64_t t0 = 0; t0 < N; t0 += C::TR, ++nt) {
+    float* X0 = tiles + (nt & 1) * 2 * TD;
+    float* X1 = X0 + TD;
+    float* rinv = rinv_all + (nt & 1) * C::TR;
+    put_tile<D>(X0, rinv, ra, N, t0, kKey, vrow, eps, nullptr);
+    put_tile<D>(X1, rinv, rb4, N, t0, kRaw, vrow, eps, nullptr);
     __syncthreads();
+    if (t0 + C::TR < N) {
+      fetch_tile<T, D>(ra, K, base, p.sn, N, t0 + C::TR);
+      fetch_tile<T, D>(rb4, V, base, p.sn, N, t0 + C::TR);
+    }
     {
       float o[C::RR][C::RC];
       rowout_tile<D>(o, X1, Bt, rb, cb);  // dK~ = V dA^T
@@ -403,11 +461,11 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
         const int r = rb + 16 * k;
         const int64_t row = t0 + r;
         const bool f = row < N && (vrow == nullptr || vrow[row] != 0);
-        const float d = row_dot<D>(o[k], X0 + r * D, cb);
+        const float d = row_dot<D>(o[k], X0 + r * C::LDT, cb);
         const float iv = rinv[r];
 #pragma unroll
         for (int g = 0; g < C::RC / 4; ++g) {
-          const float4 q = *reinterpret_cast<const float4*>(X0 + r * D + 64 * g + 4 * cb);
+          const float4 q = *reinterpret_cast<const float4*>(X0 + r * C::LDT + 64 * g + 4 * cb);
           o[k][4 * g] = f ? (o[k][4 * g] - d * q.x) * iv : 0.f;
           o[k][4 * g + 1] = f ? (o[k][4 * g + 1] - d * q.y) * iv : 0.f;
           o[k][4 * g + 2] = f ? (o[k][4 * g + 2] - d * q.z) * iv : 0.f;
@@ -428,7 +486,6 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
         if (row < N) store_row<T, D>(dV + base + row * p.sn, o[k], cb);
       }
     }
-    __syncthreads();
   }
 }
 
