@@ -62,6 +62,11 @@ WORKLOADS = {
                     "BASELINE config #5 point: cosine-attn fwd+bwd, N=4096, H=1, d_h=128, B=256, fp32 "
                     "(register-tiled FP32-pipe kernels), left-padded mask"),
 }
+# bf16 in HBM (fp32 arithmetic) points of config #5: the same shapes, half the bytes
+for _name in ("long4k", "long4k_d64", "long4k_d128"):
+    _w = WORKLOADS[_name]
+    WORKLOADS[_name + "_bf16"] = _w[:6] + (_w[6].replace("fp32", "bf16 in HBM (fp32 arithmetic)"),)
+WORKLOAD_DTYPE = {n: "bf16" for n in WORKLOADS if n.endswith("_bf16")}
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -81,8 +86,10 @@ def pipe_flops(B, H, N, D):
     return B * H * (4 * N * D * D + 7 * N * D), B * H * (8 * N * D * D + 12 * N * D)
 
 
-def kernel_path(path, N, D):
+def kernel_path(path, N, D, dname="f32"):
     """The kernels the library picks for this shape (cotten_capi.cu launch_*_t)."""
+    if dname == "bf16" and D == 32:
+        return "fp32-rt register-tiled FP32 pipe (kernels_rt.cuh)"
     if D == 32 and path == "tcgen05" and N > 64:
         return "tcgen05 (kernels_tc.cuh)"
     if D == 32:
@@ -200,6 +207,8 @@ def run_ours(args, world, rank, local):
     from paper_2602_06935_b200 import _lib, inputs, ops
 
     total_b, N, H, D, layers, strong, desc = WORKLOADS[args.workload]
+    dname = WORKLOAD_DTYPE.get(args.workload, "f32")
+    tdtype = torch.bfloat16 if dname == "bf16" else torch.float32
     lo, hi = shard(total_b, rank, world) if strong else (0, total_b)
     B = hi - lo
     global_b = total_b if strong else total_b * world
@@ -209,7 +218,7 @@ def run_ours(args, world, rank, local):
     # Inputs resident in HBM before the timed region (distinct per layer / rank).
     L = []
     for layer in range(layers):
-        t = inputs.make_device(B, H, N, D, seed=1000 * layer + rank, device=dev)
+        t = inputs.make_device(B, H, N, D, seed=1000 * layer + rank, dtype=tdtype, device=dev)
         valid = torch.from_numpy(inputs.left_padded_mask(B, N, 1000 * layer + rank)).to(dev)
         t.update(valid=valid,
                  out=torch.empty_like(t["q"]), S=torch.empty(B * H, D, D, device=dev),
@@ -364,7 +373,7 @@ def run_ours(args, world, rank, local):
     ms_per_step = total_ms / args.steps
     value = global_b * args.steps / (total_ms / 1e3)
 
-    fwd_bytes, bwd_bytes = algorithmic_bytes(B, H, N, D)
+    fwd_bytes, bwd_bytes = algorithmic_bytes(B, H, N, D, elt=2 if dname == "bf16" else 4)
     peak, peak_src = load_peaks()
     fwd_avg = statistics.mean(fwd_ms) / 1e3
     bwd_avg = statistics.mean(bwd_ms) / 1e3
@@ -375,12 +384,12 @@ def run_ours(args, world, rank, local):
     res = {
         "metric": METRIC, "value": value, "unit": "seq/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": dname,
         "data": "synthetic U(-1,1) (mix_seed per shape, bench.cpp:21-26,50), left-padded masks",
         "config": {"workload": desc, "name": args.workload, "global_batch": global_b,
                    "batch_per_gpu": B, "seq_len": N, "heads": H, "head_dim": D, "model_dim": H * D,
                    "layers": layers, "parallelism": f"dp{world} (batch x head shards)",
-                   "kernel_path": kernel_path(args.path, N, D),
+                   "kernel_path": kernel_path(args.path, N, D, dname),
                    "launch": "eager" if args.no_graph else ("one CUDA graph per op call, replayed back to back "
                                                               "(events at step boundaries); per-op kernel times "
                                                               "from a separately marked pass"),
@@ -396,7 +405,7 @@ def run_ours(args, world, rank, local):
         "gpu_launches": gpu_launches,
         "clocks": clocks,
     }
-    if D != 32:  # FP32-pipe kernels: compute at peak bounds them, not HBM (north star: max of both)
+    if D != 32 or dname == "bf16":  # FP32-pipe kernels: compute at peak bounds them, not HBM (north star: max of both)
         ff, fb = pipe_flops(B, H, N, D)
         t_f = max(ff / FP32_PEAK_FLOPS, fwd_bytes / (peak * 1e9))
         t_b = max(fb / FP32_PEAK_FLOPS, bwd_bytes / (peak * 1e9))
@@ -420,9 +429,11 @@ def run_ours(args, world, rank, local):
         except Exception:
             pass
 
-    if not args.no_e2e:
+    if not args.no_e2e and dname == "bf16":
+        res["e2e"] = {"value": None, "note": "bf16 points are device-resident kernel measurements only"}
+    elif not args.no_e2e:
         res["e2e"] = run_e2e(args, world, B, N, H, D, layers, global_b)
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and dname == "f32":
         res["cpu_baseline"] = run_cpu_baseline(args, N, H, D, layers, B)
     return res
 

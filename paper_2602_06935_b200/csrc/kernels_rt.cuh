@@ -43,10 +43,14 @@ constexpr int kThreads = 256;
 
 template <int D>
 struct Cfg {
-  static constexpr int RA = D / 16;             // state rows per thread
-  static constexpr int RC = D / 16;             // state / output columns per thread
-  static constexpr int RR = kThreads / D;       // output rows per thread (4 / 2)
-  static constexpr int TR = 16 * RR;            // tile rows (64 / 32)
+  // thread tid = (row index) * CB + cb: cb picks the 4-column groups
+  // cb + CB g of a row (state and outputs alike)
+  static constexpr int CB = D / 4 < 16 ? D / 4 : 16;  // column-group threads (8 / 16 / 16)
+  static constexpr int RB = kThreads / CB;             // distinct row indices (32 / 16 / 16)
+  static constexpr int RC = D / CB;                    // columns per thread (4 / 4 / 8)
+  static constexpr int RA = D * D / (kThreads * RC);   // state rows per thread (1 / 4 / 8)
+  static constexpr int RR = 16 / RC;                   // output rows per thread (4 / 4 / 2)
+  static constexpr int TR = RB * RR;                   // tile rows (128 / 64 / 32)
   static constexpr int F4 = D / 4;              // 4-element groups per row
   static constexpr int LD = TR * F4 / kThreads; // 4-element loads per thread per tile
   static constexpr int kFlushTiles = 512 / TR;  // running-sum flush period (512 rows)
@@ -136,14 +140,18 @@ __device__ __forceinline__ void reduce_tile(float (&acc)[Cfg<D>::RA][Cfg<D>::RC]
 #pragma unroll 2
   for (int r = 0; r < rows; ++r) {
     float xa[C::RA], yc[C::RC];
+    if constexpr (C::RA == 1) {
+      xa[0] = x[r * C::LDT + ab];
+    } else {
 #pragma unroll
-    for (int g = 0; g < C::RA / 4; ++g) {
-      const float4 u = *reinterpret_cast<const float4*>(x + r * C::LDT + 64 * g + 4 * ab);
-      xa[4 * g] = u.x; xa[4 * g + 1] = u.y; xa[4 * g + 2] = u.z; xa[4 * g + 3] = u.w;
+      for (int g = 0; g < C::RA / 4; ++g) {
+        const float4 u = *reinterpret_cast<const float4*>(x + r * C::LDT + 64 * g + 4 * ab);
+        xa[4 * g] = u.x; xa[4 * g + 1] = u.y; xa[4 * g + 2] = u.z; xa[4 * g + 3] = u.w;
+      }
     }
 #pragma unroll
     for (int g = 0; g < C::RC / 4; ++g) {
-      const float4 u = *reinterpret_cast<const float4*>(y + r * C::LDT + 64 * g + 4 * cb);
+      const float4 u = *reinterpret_cast<const float4*>(y + r * C::LDT + 4 * (cb + C::CB * g));
       yc[4 * g] = u.x; yc[4 * g + 1] = u.y; yc[4 * g + 2] = u.z; yc[4 * g + 3] = u.w;
     }
 #pragma unroll
@@ -165,10 +173,10 @@ __device__ __forceinline__ void flush_state(float (&acc)[Cfg<D>::RA][Cfg<D>::RC]
   using C = Cfg<D>;
 #pragma unroll
   for (int i = 0; i < C::RA; ++i) {
-    const int a = 64 * (i / 4) + 4 * ab + (i % 4);
+    const int a = C::RA == 1 ? ab : 64 * (i / 4) + 4 * ab + (i % 4);
 #pragma unroll
     for (int g = 0; g < C::RC / 4; ++g) {
-      float4* q = reinterpret_cast<float4*>(run + a * D + 64 * g + 4 * cb);
+      float4* q = reinterpret_cast<float4*>(run + a * D + 4 * (cb + C::CB * g));
       float4 v = *q;
       v.x += acc[i][4 * g]; v.y += acc[i][4 * g + 1]; v.z += acc[i][4 * g + 2]; v.w += acc[i][4 * g + 3];
       *q = v;
@@ -191,13 +199,13 @@ __device__ __forceinline__ void rowout_tile(float (&out)[Cfg<D>::RR][Cfg<D>::RC]
   for (int x = 0; x < D; x += 4) {
     float4 xr[C::RR];
 #pragma unroll
-    for (int k = 0; k < C::RR; ++k) xr[k] = *reinterpret_cast<const float4*>(X + (rb + 16 * k) * C::LDT + x);
+    for (int k = 0; k < C::RR; ++k) xr[k] = *reinterpret_cast<const float4*>(X + (rb + C::RB * k) * C::LDT + x);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float m[C::RC];
 #pragma unroll
       for (int g = 0; g < C::RC / 4; ++g) {
-        const float4 u = *reinterpret_cast<const float4*>(M + (x + e) * D + 64 * g + 4 * cb);
+        const float4 u = *reinterpret_cast<const float4*>(M + (x + e) * D + 4 * (cb + C::CB * g));
         m[4 * g] = u.x; m[4 * g + 1] = u.y; m[4 * g + 2] = u.z; m[4 * g + 3] = u.w;
       }
 #pragma unroll
@@ -222,14 +230,14 @@ __device__ __forceinline__ float row_dot(const float (&o)[Cfg<D>::RC], const flo
   float d = 0.f;
 #pragma unroll
   for (int g = 0; g < C::RC / 4; ++g) {
-    const float4 u = *reinterpret_cast<const float4*>(xrow + 64 * g + 4 * cb);
+    const float4 u = *reinterpret_cast<const float4*>(xrow + 4 * (cb + C::CB * g));
     d = fmaf(o[4 * g], u.x, d);
     d = fmaf(o[4 * g + 1], u.y, d);
     d = fmaf(o[4 * g + 2], u.z, d);
     d = fmaf(o[4 * g + 3], u.w, d);
   }
 #pragma unroll
-  for (int s = 8; s > 0; s >>= 1) d += __shfl_xor_sync(0xffffffffu, d, s);
+  for (int s = C::CB / 2; s > 0; s >>= 1) d += __shfl_xor_sync(0xffffffffu, d, s);
   return d;
 }
 
@@ -238,7 +246,7 @@ __device__ __forceinline__ void store_row(T* dst, const float (&o)[Cfg<D>::RC], 
   using C = Cfg<D>;
 #pragma unroll
   for (int g = 0; g < C::RC / 4; ++g)
-    st4(dst + 64 * g + 4 * cb, o[4 * g], o[4 * g + 1], o[4 * g + 2], o[4 * g + 3]);
+    st4(dst + 4 * (cb + C::CB * g), o[4 * g], o[4 * g + 1], o[4 * g + 2], o[4 * g + 3]);
 }
 
 template <typename T, int D>
@@ -263,7 +271,7 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
   }
   const float scale = (float)exp(-p.m * log((double)true_n));  // :303-304, in fp64
   const float eps = (float)p.eps;
-  const int tid = threadIdx.x, ab = tid >> 4, cb = tid & 15;
+  const int tid = threadIdx.x, ab = tid / C::CB, cb = tid % C::CB;
   for (int e = tid; e < D * D; e += kThreads) Ssm[e] = 0.f;
 
   float acc[C::RA][C::RC];
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
   if (p.out == nullptr && norms == nullptr) return;
 
   T* O = static_cast<T*>(p.out);
-  const int rb = tid >> 4;
+  const int rb = tid / C::CB;
   fetch_tile<T, D>(ra, Q, base, p.sn, N, 0);
   nt = 0;
   for (int64_t t0 = 0; t0 < N; t0 += C::TR, ++nt) {
@@ -315,7 +323,7 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
       rowout_tile<D>(o, X0, Ssm, rb, cb);
 #pragma unroll
       for (int k = 0; k < C::RR; ++k) {
-        const int64_t row = t0 + rb + 16 * k;
+        const int64_t row = t0 + rb + C::RB * k;
 #pragma unroll
         for (int j = 0; j < C::RC; ++j) o[k][j] *= scale;
         if (row < N) store_row<T, D>(O + base + row * p.sn, o[k], cb);
@@ -354,7 +362,7 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
   const double log_n = log((double)true_n);  // :402-403
   const float scale = (float)exp(-p.m * log_n);
   const float eps = (float)p.eps;
-  const int tid = threadIdx.x, ab = tid >> 4, cb = tid & 15, rb = tid >> 4;
+  const int tid = threadIdx.x, ab = tid / C::CB, cb = tid % C::CB, rb = ab;
 
   // S^T into Bt (Bt[c][a] = S[a][c], conflict-free smem writes), G = 0
   const float* gS = static_cast<const float*>(p.saved_S) + unit * (int64_t)D * D;
@@ -395,14 +403,14 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
     rowout_tile<D>(o, X1, Bt, rb, cb);  // dO S^T
 #pragma unroll
     for (int k = 0; k < C::RR; ++k) {
-      const int r = rb + 16 * k;
+      const int r = rb + C::RB * k;
 #pragma unroll
       for (int j = 0; j < C::RC; ++j) o[k][j] *= scale;
       const float d = row_dot<D>(o[k], X0 + r * C::LDT, cb);
       const float iv = rinv[r];
 #pragma unroll
       for (int g = 0; g < C::RC / 4; ++g) {
-        const float4 q = *reinterpret_cast<const float4*>(X0 + r * C::LDT + 64 * g + 4 * cb);
+        const float4 q = *reinterpret_cast<const float4*>(X0 + r * C::LDT + 4 * (cb + C::CB * g));
         o[k][4 * g] = (o[k][4 * g] - d * q.x) * iv;
         o[k][4 * g + 1] = (o[k][4 * g + 1] - d * q.y) * iv;
         o[k][4 * g + 2] = (o[k][4 * g + 2] - d * q.z) * iv;
@@ -458,14 +466,14 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
       rowout_tile<D>(o, X1, Bt, rb, cb);  // dK~ = V dA^T
 #pragma unroll
       for (int k = 0; k < C::RR; ++k) {
-        const int r = rb + 16 * k;
+        const int r = rb + C::RB * k;
         const int64_t row = t0 + r;
         const bool f = row < N && (vrow == nullptr || vrow[row] != 0);
         const float d = row_dot<D>(o[k], X0 + r * C::LDT, cb);
         const float iv = rinv[r];
 #pragma unroll
         for (int g = 0; g < C::RC / 4; ++g) {
-          const float4 q = *reinterpret_cast<const float4*>(X0 + r * C::LDT + 64 * g + 4 * cb);
+          const float4 q = *reinterpret_cast<const float4*>(X0 + r * C::LDT + 4 * (cb + C::CB * g));
           o[k][4 * g] = f ? (o[k][4 * g] - d * q.x) * iv : 0.f;
           o[k][4 * g + 1] = f ? (o[k][4 * g + 1] - d * q.y) * iv : 0.f;
           o[k][4 * g + 2] = f ? (o[k][4 * g + 2] - d * q.z) * iv : 0.f;
@@ -479,7 +487,7 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
       rowout_tile<D>(o, X0, Bn, rb, cb);  // dV = K~ dA
 #pragma unroll
       for (int k = 0; k < C::RR; ++k) {
-        const int64_t row = t0 + rb + 16 * k;
+        const int64_t row = t0 + rb + C::RB * k;
         const bool f = row < N && (vrow == nullptr || vrow[row] != 0);
 #pragma unroll
         for (int j = 0; j < C::RC; ++j) o[k][j] = f ? o[k][j] : 0.f;
@@ -495,7 +503,8 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
 template <typename T>
 inline bool rt_supported(const OpParams& p, bool bwd) {
   if (sizeof(T) == 8) return false;
-  if (p.D != 64 && p.D != 128) return false;
+  // d_h 64 / 128 (f32, bf16); d_h 32 only for bf16 (f32 d_h = 32 runs on the tensor cores)
+  if (p.D != 64 && p.D != 128 && !(p.D == 32 && sizeof(T) == 2)) return false;
   if (p.N < 1 || p.N > (int64_t)1 << 30) return false;
   const uintptr_t align = sizeof(T) == 4 ? 16 : 8;
   if (p.sn % 4 || p.sh % 4 || p.sb % 4) return false;
@@ -514,7 +523,8 @@ inline void launch_rt_fwd(const OpParams& p, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)(p.B * p.H), rt::kThreads, smem, st>>>(p);
   };
-  if (p.D == 64) go(rt::cos_fwd_rt<T, 64>, rt::Cfg<64>::fwd_smem);
+  if (p.D == 32) go(rt::cos_fwd_rt<T, 32>, rt::Cfg<32>::fwd_smem);
+  else if (p.D == 64) go(rt::cos_fwd_rt<T, 64>, rt::Cfg<64>::fwd_smem);
   else go(rt::cos_fwd_rt<T, 128>, rt::Cfg<128>::fwd_smem);
 }
 template <typename T>
@@ -523,7 +533,8 @@ inline void launch_rt_bwd(const OpParams& p, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)(p.B * p.H), rt::kThreads, smem, st>>>(p);
   };
-  if (p.D == 64) go(rt::cos_bwd_rt<T, 64>, rt::Cfg<64>::bwd_smem);
+  if (p.D == 32) go(rt::cos_bwd_rt<T, 32>, rt::Cfg<32>::bwd_smem);
+  else if (p.D == 64) go(rt::cos_bwd_rt<T, 64>, rt::Cfg<64>::bwd_smem);
   else go(rt::cos_bwd_rt<T, 128>, rt::Cfg<128>::bwd_smem);
 }
 

@@ -23,21 +23,24 @@
 //     products), A = the chunk (K-major SW128), B = the 32x32 state operand
 //     (S, S^T, dA or dA^T, split hi/lo) written by the workers.
 //
-// Warp roles (384 threads, one CTA per SM, persistent over units):
-//   warps 0-7  two worker groups of 4 warps; group g takes chunks i = g (mod 2)
-//              and thread t owns row t of its chunk (= TMEM lane t): row norms,
-//              masking, hi/lo split (hi in place in the TMA stage, lo into the
-//              group's lo buffer), then the epilogue: TMEM -> registers ->
-//              scale / Jacobian / mask -> the chunk's own TMA stage as staging
-//              -> TMA store.  While one group waits on its MMAs the other
-//              splits or stores, so each SMSP always has a worker to issue.
-//   warp 8     TMA producer: raw chunks into a 4-stage ring.
-//   warp 9     MMA issuer (one elected thread) + TMEM allocator.
+// Warp roles (384 threads, one CTA per SM, persistent over units; ring of 3
+// slots, slot = item % 3, each = one TMA stage + one lo buffer + one TMEM
+// buffer; an "item" is one 128-row chunk of one pass of one unit):
+//   warps 0-3  splitter group: thread t owns row t of the chunk (= TMEM lane t):
+//              row norms, masking, hi/lo split (lo into the slot's lo buffer,
+//              hi in place or into TMEM as the MMA's A operand), the per-row
+//              1/norm parked in TMEM for the epiloguer.
+//   warps 4-7  epiloguer group: TMEM -> registers -> scale / Jacobian / mask
+//              -> staged in the slot's lo buffer for the store warp; once per
+//              unit the S / G epilogue (saved S, dm in a fixed order, the
+//              state operands S / dA hi/lo in shared memory).
+//   warp 8     TMA producer: raw chunks into the ring.
+//   warp 9     MMA issuer (converged warp, one elect.sync lane) + TMEM allocator.
 //   warp 10    mask warp: up to two units ahead, valid bytes -> bitmask,
 //              true_n, s = exp(-m ln n), coef = -ln(n) s in fp64
 //              (attention.cpp:303-304, :402-408).
-//   warp 11    store warp: TMA-stores each chunk's staged outputs and hands
-//              the stage back to the producer once the store has read it.
+//   warp 11    store warp: TMA-stores each chunk's staged outputs and frees the
+//              slot's lo buffer once the store has read it.
 // Nothing but the outputs, S (4 KB per unit) and dm reach HBM.
 #pragma once
 #include <cuda.h>

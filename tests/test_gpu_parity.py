@@ -232,6 +232,18 @@ def test_head_dim_128_random_mask(dtype):
     assert_parity(res, oracle_for(res["inputs"], valid, 1.0, 1e-6), valid, dtype)
 
 
+@pytest.mark.parametrize("D", [32, 64, 128])
+@pytest.mark.parametrize("N", [5, 129, 1000])
+def test_bf16_register_tiled_seq_lens(D, N):
+    """bf16 in HBM on kernels_rt.cuh (d_h 32 / 64 / 128): tile edges of the
+    128 / 64 / 32-row tiles, random masks."""
+    B, H = 3, 2
+    h = inputs.make_host(B, H, N, D, seed=7 * N + D)
+    valid = inputs.random_mask(B, N, N + D)
+    res = run_gpu(h, valid, 1.0, 1e-6, "bf16")
+    assert_parity(res, oracle_for(res["inputs"], valid, 1.0, 1e-6), valid, "bf16")
+
+
 @pytest.mark.parametrize("D", [64, 128])
 def test_nan_in_padded_key_rows_never_read_rt(D):
     B, H, N = 3, 2, 150
