@@ -333,8 +333,18 @@ void host_check_mask(const Layout& L, const uint8_t* valid, const char* what) {
 }
 
 // Per-thread staging state for the host entry points.
+// Staging streams of the host entry points: the batch is cut into slices of
+// whole sequences and slice i's uploads, kernels and downloads are queued on
+// pipe[i % kPipe], so uploads of one slice, kernels of the next and downloads
+// of the previous overlap (the two PCIe directions run on separate copy
+// engines; end to end the host calls are PCIe-bound).
+constexpr int kPipe = 3;
+constexpr size_t kSliceBytes = size_t(2) << 20;  // min bytes per tensor per slice
+constexpr int kMaxSlices = 8;
+
 struct HostCtx {
   cudaStream_t stream = nullptr;
+  cudaStream_t pipe[kPipe] = {};
   int dev = -1;
   std::vector<void*> bufs;
   std::vector<size_t> sizes;
@@ -343,6 +353,8 @@ struct HostCtx {
     for (void* b : bufs)
       if (b) cudaFree(b);
     if (stream) cudaStreamDestroy(stream);
+    for (cudaStream_t p : pipe)
+      if (p) cudaStreamDestroy(p);
   }
   void ensure() {
     int cur = 0;
@@ -351,9 +363,12 @@ struct HostCtx {
       bufs.assign(12, nullptr);
       sizes.assign(12, 0);
       stream = nullptr;
+      for (cudaStream_t& p : pipe) p = nullptr;
       dev = cur;
     }
     if (stream == nullptr) COTTEN_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    for (cudaStream_t& p : pipe)
+      if (p == nullptr) COTTEN_CUDA(cudaStreamCreateWithFlags(&p, cudaStreamNonBlocking));
   }
   void* buf(int slot, size_t need) {
     if (need > sizes[slot]) {
@@ -376,6 +391,37 @@ void* h2d(int slot, const void* src, size_t bytes) {
 }
 void d2h(void* dst, const void* src, size_t bytes) {
   if (dst) COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g_host.stream));
+}
+
+// Slices of whole sequences for the pipelined host path (f64 keeps the single
+// stream: its large-d_h backward uses a shared global workspace).
+struct Slices {
+  int64_t per = 0;  // sequences per slice
+  int n = 1;
+};
+Slices plan_slices(const Layout& L, size_t tensor_bytes) {
+  Slices sl;
+  int n = (int)std::min<size_t>(kMaxSlices, std::max<size_t>(1, tensor_bytes / kSliceBytes));
+  if (L.dtype == COTTEN_F64) n = 1;
+  n = (int)std::min<int64_t>(n, L.B);
+  sl.per = (L.B + n - 1) / n;
+  sl.n = (int)((L.B + sl.per - 1) / sl.per);
+  return sl;
+}
+void pipe_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (src && bytes) COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+}
+void pipe_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (dst && bytes) COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+}
+void pipe_sync() {
+  for (cudaStream_t p : g_host.pipe) COTTEN_CUDA(cudaStreamSynchronize(p));
+}
+template <typename P>
+P* at(P* base, int64_t bytes) {
+  return base ? reinterpret_cast<P*>(reinterpret_cast<uint8_t*>(const_cast<void*>(
+                    static_cast<const void*>(base))) + bytes)
+              : nullptr;
 }
 
 }  // namespace
@@ -439,19 +485,34 @@ int cotten_fwd_host(const cotten_desc* desc, const void* q, const void* k, const
     const size_t tb = L.span() * elem_size(L.dtype);
     const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
     const size_t nbytes = L.units() * 2 * L.N * acc_size(L.dtype);
-    void* dq = h2d(kQ, q, tb);
-    void* dk = h2d(kK, k, tb);
-    void* dv = h2d(kV, v, tb);
-    const uint8_t* dmask =
-        valid ? static_cast<const uint8_t*>(h2d(kMask, valid, (L.B - 1) * L.msb + L.N)) : nullptr;
+    const size_t es = elem_size(L.dtype), as = acc_size(L.dtype);
+    void* dq = g_host.buf(kQ, tb);
+    void* dk = g_host.buf(kK, tb);
+    void* dv = g_host.buf(kV, tb);
+    uint8_t* dmask = valid ? static_cast<uint8_t*>(g_host.buf(kMask, (L.B - 1) * L.msb + L.N)) : nullptr;
     void* dout = out ? g_host.buf(kO, tb) : nullptr;
     void* dS = saved_S ? g_host.buf(kS, sbytes) : nullptr;
     void* dN = saved_norms ? g_host.buf(kNorms, nbytes) : nullptr;
-    device_fwd(L, dq, dk, dv, dmask, m, dout, dS, dN, g_host.stream);
-    d2h(out, dout, tb);
-    d2h(saved_S, dS, sbytes);
-    d2h(saved_norms, dN, nbytes);
-    COTTEN_CUDA(cudaStreamSynchronize(g_host.stream));
+    const Slices sl = plan_slices(L, tb);
+    for (int i = 0; i < sl.n; ++i) {  // pipelined slices of whole sequences
+      cudaStream_t st = g_host.pipe[i % kPipe];
+      const int64_t b0 = i * sl.per, nb = std::min(sl.per, L.B - b0);
+      Layout Lc = L;
+      Lc.B = nb;
+      const size_t off = b0 * L.sb * es, len = nb * L.sb * es;
+      const size_t soff = b0 * L.H * L.D * L.D * as, slen = nb * L.H * L.D * L.D * as;
+      const size_t noff = b0 * L.H * 2 * L.N * as, nlen = nb * L.H * 2 * L.N * as;
+      pipe_h2d(at(dq, off), at(q, off), len, st);
+      pipe_h2d(at(dk, off), at(k, off), len, st);
+      pipe_h2d(at(dv, off), at(v, off), len, st);
+      if (dmask) pipe_h2d(dmask + b0 * L.msb, valid + b0 * L.msb, (nb - 1) * L.msb + L.N, st);
+      device_fwd(Lc, at(dq, off), at(dk, off), at(dv, off), dmask ? dmask + b0 * L.msb : nullptr, m,
+                 at(dout, off), at(dS, soff), at(dN, noff), st);
+      pipe_d2h(at(out, off), at(dout, off), out ? len : 0, st);
+      pipe_d2h(at(saved_S, soff), at(dS, soff), saved_S ? slen : 0, st);
+      pipe_d2h(at(saved_norms, noff), at(dN, noff), saved_norms ? nlen : 0, st);
+    }
+    pipe_sync();
   });
 }
 
@@ -468,24 +529,50 @@ int cotten_bwd_host(const cotten_desc* desc, const void* q, const void* k, const
     g_host.ensure();
     const size_t tb = L.span() * elem_size(L.dtype);
     const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
-    void* gq = h2d(kQ, q, tb);
-    void* gk = h2d(kK, k, tb);
-    void* gv = h2d(kV, v, tb);
-    void* gdo = h2d(kDO, d_out, tb);
-    const uint8_t* dmask =
-        valid ? static_cast<const uint8_t*>(h2d(kMask, valid, (L.B - 1) * L.msb + L.N)) : nullptr;
-    const void* gS = saved_S ? h2d(kS, saved_S, sbytes) : nullptr;
+    const size_t es = elem_size(L.dtype), as = acc_size(L.dtype);
+    void* gq = g_host.buf(kQ, tb);
+    void* gk = g_host.buf(kK, tb);
+    void* gv = g_host.buf(kV, tb);
+    void* gdo = g_host.buf(kDO, tb);
+    uint8_t* dmask = valid ? static_cast<uint8_t*>(g_host.buf(kMask, (L.B - 1) * L.msb + L.N)) : nullptr;
+    void* gS = g_host.buf(kS, sbytes);  // uploaded, or recomputed per slice when not given
     void* gdq = g_host.buf(kDQ, tb);
     void* gdk = g_host.buf(kDK, tb);
     void* gdv = g_host.buf(kDV, tb);
     double* gdm = static_cast<double*>(g_host.buf(kDm, (L.units() + 1) * sizeof(double)));
-    device_bwd(L, gq, gk, gv, dmask, m, gdo, gS, gdq, gdk, gdv, gdm, gdm + L.units(),
-               g_host.stream);
-    d2h(dq, gdq, tb);
-    d2h(dk, gdk, tb);
-    d2h(dv, gdv, tb);
-    d2h(dm_unit, gdm, L.units() * sizeof(double));
-    d2h(dm_total, gdm + L.units(), sizeof(double));
+    const Slices sl = plan_slices(L, tb);
+    for (int i = 0; i < sl.n; ++i) {  // pipelined slices of whole sequences
+      cudaStream_t st = g_host.pipe[i % kPipe];
+      const int64_t b0 = i * sl.per, nb = std::min(sl.per, L.B - b0);
+      Layout Lc = L;
+      Lc.B = nb;
+      const size_t off = b0 * L.sb * es, len = nb * L.sb * es;
+      const size_t soff = b0 * L.H * L.D * L.D * as, slen = nb * L.H * L.D * L.D * as;
+      const uint8_t* mk = dmask ? dmask + b0 * L.msb : nullptr;
+      pipe_h2d(at(gq, off), at(q, off), len, st);
+      pipe_h2d(at(gk, off), at(k, off), len, st);
+      pipe_h2d(at(gv, off), at(v, off), len, st);
+      pipe_h2d(at(gdo, off), at(d_out, off), len, st);
+      if (dmask) pipe_h2d(dmask + b0 * L.msb, valid + b0 * L.msb, (nb - 1) * L.msb + L.N, st);
+      if (saved_S)
+        pipe_h2d(at(gS, soff), at(saved_S, soff), slen, st);
+      else  // the state from an S-only forward of this slice
+        device_fwd(Lc, at(gq, off), at(gk, off), at(gv, off), mk, m, nullptr, at(gS, soff), nullptr, st);
+      // dm per unit only: the batch total is one fixed-order sum after the slices
+      device_bwd(Lc, at(gq, off), at(gk, off), at(gv, off), mk, m, at(gdo, off), at(gS, soff),
+                 at(gdq, off), at(gdk, off), at(gdv, off), gdm + b0 * L.H, nullptr, st);
+      pipe_d2h(at(dq, off), at(gdq, off), len, st);
+      pipe_d2h(at(dk, off), at(gdk, off), len, st);
+      pipe_d2h(at(dv, off), at(gdv, off), len, st);
+      pipe_d2h(dm_unit ? dm_unit + b0 * L.H : nullptr, gdm + b0 * L.H, nb * L.H * sizeof(double), st);
+    }
+    pipe_sync();
+    if (dm_total) {  // the same partition and tree as the single-launch total (bit-identical)
+      dm_reduce_kernel<<<1, 256, 0, g_host.stream>>>(gdm, L.units(), gdm + L.units());
+      g_launches += 1;
+      COTTEN_CUDA(cudaGetLastError());
+      d2h(dm_total, gdm + L.units(), sizeof(double));
+    }
     COTTEN_CUDA(cudaStreamSynchronize(g_host.stream));
   });
 }

@@ -378,3 +378,39 @@ def test_full_size_properties(config):
     dms, dms_ref = np.array(dms), np.array(dms_ref)
     assert np.abs(dms - dms_ref).max() / np.abs(dms_ref).max() <= 1e-5
     assert dm_total.item() == pytest.approx(dm_unit.sum().item(), rel=1e-9)
+
+
+@pytest.mark.parametrize("D,dtype", [(32, "f32"), (64, "f32"), (32, "bf16")])
+def test_host_entry_slices_match_device_entry(D, dtype):
+    """cotten_fwd_host / cotten_bwd_host stage the batch in pipelined slices of
+    whole sequences (3 streams); the results must equal the single device call
+    bit for bit: out, S, dQ, dK, dV, dm per unit and the fixed-order dm total,
+    with the state given and recomputed, and an uneven last slice."""
+    import ctypes
+    torch = torch_mod()
+    B, H, N = (301, 2, 200) if D == 32 else (151, 2, 200)
+    h = inputs.make_host(B, H, N, D, seed=31)
+    valid = inputs.left_padded_mask(B, N, 31)
+    ref = run_gpu(h, valid, 1.0, 1e-6, dtype)
+    lib = _lib.load()
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+    host = {n: torch.from_numpy(h[n]).to(tdt).contiguous().pin_memory() for n in ("q", "k", "v", "d_out")}
+    vm = torch.from_numpy(valid).contiguous().pin_memory()
+    outs = {n: torch.empty((B, H, N, D), dtype=tdt).pin_memory() for n in ("out", "dq", "dk", "dv")}
+    S = torch.empty((B * H, D, D), dtype=torch.float32).pin_memory()
+    dm_unit = torch.empty(B * H, dtype=torch.float64).pin_memory()
+    dm_total = torch.empty(1, dtype=torch.float64).pin_memory()
+    desc = _lib.make_desc(B, H, N, D, dtype, 1e-6)
+    p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.check(lib.cotten_fwd_host(ctypes.byref(desc), p(host["q"]), p(host["k"]), p(host["v"]), p(vm),
+                                   1.0, p(outs["out"]), p(S), None))
+    for saved in (S, None):
+        _lib.check(lib.cotten_bwd_host(ctypes.byref(desc), p(host["q"]), p(host["k"]), p(host["v"]),
+                                       p(vm), 1.0, p(host["d_out"]), None if saved is None else p(saved),
+                                       p(outs["dq"]), p(outs["dk"]), p(outs["dv"]), p(dm_unit),
+                                       p(dm_total)))
+        for n in ("out", "dq", "dk", "dv"):
+            np.testing.assert_array_equal(outs[n].double().numpy(), ref[n], err_msg=n)
+        np.testing.assert_array_equal(S.double().numpy(), ref["S"])
+        np.testing.assert_array_equal(dm_unit.numpy(), ref["dm_unit"])
+        assert float(dm_total.item()) == ref["dm_total"]
