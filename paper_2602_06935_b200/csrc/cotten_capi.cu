@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <type_traits>
@@ -341,6 +342,21 @@ void host_check_mask(const Layout& L, const uint8_t* valid, const char* what) {
 constexpr int kPipe = 3;
 constexpr size_t kSliceBytes = size_t(2) << 20;  // min bytes per tensor per slice
 constexpr int kMaxSlices = 8;
+// COTTEN_HOST_SLICE_KB / COTTEN_HOST_MAX_SLICES override the two (tuning)
+size_t slice_bytes() {
+  static const size_t v = [] {
+    const char* e = std::getenv("COTTEN_HOST_SLICE_KB");
+    return e ? std::max<size_t>(64, std::strtoull(e, nullptr, 10)) << 10 : kSliceBytes;
+  }();
+  return v;
+}
+int max_slices() {
+  static const int v = [] {
+    const char* e = std::getenv("COTTEN_HOST_MAX_SLICES");
+    return e ? std::max(1, std::atoi(e)) : kMaxSlices;
+  }();
+  return v;
+}
 
 struct HostCtx {
   cudaStream_t stream = nullptr;
@@ -401,7 +417,7 @@ struct Slices {
 };
 Slices plan_slices(const Layout& L, size_t tensor_bytes) {
   Slices sl;
-  int n = (int)std::min<size_t>(kMaxSlices, std::max<size_t>(1, tensor_bytes / kSliceBytes));
+  int n = (int)std::min<size_t>(max_slices(), std::max<size_t>(1, tensor_bytes / slice_bytes()));
   if (L.dtype == COTTEN_F64) n = 1;
   n = (int)std::min<int64_t>(n, L.B);
   sl.per = (L.B + n - 1) / n;
