@@ -267,6 +267,29 @@ def test_bnhd_strided_layout_equals_contiguous():
         np.testing.assert_array_equal(a[n], b[n])
 
 
+@pytest.mark.parametrize("D,dtype", [(64, "f32"), (128, "f32"), (32, "bf16"), (64, "bf16")])
+def test_bnhd_strided_layout_register_tiled(D, dtype):
+    """The register-tiled kernels read a [B][N][H*D] projection output in
+    place (stride_n = H*D): identical results to the contiguous layout."""
+    B, H, N = 4, 2, 150
+    h = inputs.make_host(B, H, N, D, seed=40 + D)
+    valid = inputs.left_padded_mask(B, N, 40)
+    a = run_gpu(h, valid, 1.0, 1e-6, dtype, layout="bhnd")
+    b = run_gpu(h, valid, 1.0, 1e-6, dtype, layout="bnhd")
+    for n in ("out", "dq", "dk", "dv"):
+        np.testing.assert_array_equal(a[n], b[n])
+
+
+def test_head_dim_64_long_sequence_accuracy():
+    """N = 16384 at d_h = 64: the 512-row running-sum flush keeps the fp32
+    reductions within the 1e-5 bar over 32 flushes."""
+    B, H, N, D = 1, 1, 16384, 64
+    h = inputs.make_host(B, H, N, D, seed=44)
+    valid = inputs.left_padded_mask(B, N, 44)
+    res = run_gpu(h, valid, 0.75, 1e-6, "f32")
+    assert_parity(res, oracle_for(res["inputs"], valid, 0.75, 1e-6), valid, "f32")
+
+
 def test_nan_in_padded_key_rows_never_read():
     # attention.cpp:334-338: padded K rows are selected to zero, never read
     B, H, N, D = 4, 2, 64, 32
