@@ -305,6 +305,8 @@ def run_ours(args, world, rank, local):
         stream.wait_stream(cap)
         torch.cuda.synchronize()
 
+        fwd_eager, bwd_eager = fwd, bwd
+
         def fwd(t, _i=None):  # noqa: F811
             i = next(k for k in range(layers) if L[k] is t)
             graphs[("fwd", i)].replay()
@@ -315,6 +317,24 @@ def run_ours(args, world, rank, local):
             launches[0] += counts[("bwd", i)]
 
         step_launches = sum(counts.values())
+        # The whole step as one graph too: inside a graph the kernels'
+        # programmatic-dependent-launch attribute becomes a programmatic edge,
+        # so each kernel's prologue overlaps the previous kernel's tail, which
+        # separate graph launches cannot do.
+        gstep = None
+        if args.graph_scope == "step":
+            gstep = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gstep, stream=cap):
+                s_cap = torch.cuda.current_stream()
+                for i in range(layers):
+                    t = L[i]
+                    ops.forward(t["q"], t["k"], t["v"], t["valid"], m, out=t["out"], saved_S=t["S"],
+                                stream=s_cap, flags=flags)
+                for i in reversed(range(layers)):
+                    t = L[i]
+                    ops.backward(t["q"], t["k"], t["v"], t["valid"], m, t["d_out"], t["S"], t["dq"],
+                                 t["dk"], t["dv"], t["dm_unit"], dm_tot[i:i + 1], stream=s_cap,
+                                 flags=flags)
         stream.wait_stream(cap)
         torch.cuda.synchronize()
         for _ in range(2):
@@ -342,10 +362,13 @@ def run_ours(args, world, rank, local):
         else:
             # the step's per-op graphs back to back, events at the step boundaries only
             step_marks[s_][0].record(stream)
-            for i in range(layers):
-                graphs[("fwd", i)].replay()
-            for i in reversed(range(layers)):
-                graphs[("bwd", i)].replay()
+            if gstep is not None:
+                gstep.replay()
+            else:
+                for i in range(layers):
+                    graphs[("fwd", i)].replay()
+                for i in reversed(range(layers)):
+                    graphs[("bwd", i)].replay()
             launches[0] += step_launches
             if world > 1:
                 import torch.distributed as dist
@@ -354,6 +377,20 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
     gpu_launches = launches[0]
+    graph_check = None
+    if not args.no_graph:
+        # the graphs' outputs of the last timed step == a plain eager step's (same inputs)
+        names = ("out", "dq", "dk", "dv")
+        snap = [L[i][n].clone() for i in range(layers) for n in names]
+        snap_dm = dm_tot.clone()
+        for i in range(layers):
+            fwd_eager(L[i])
+        for i in reversed(range(layers)):
+            bwd_eager(L[i], i)
+        torch.cuda.synchronize()
+        graph_check = all(torch.equal(a, L[i][n]) for a, (i, n) in
+                          zip(snap, [(i, n) for i in range(layers) for n in names]))
+        graph_check = bool(graph_check and (world > 1 or torch.equal(snap_dm, dm_tot)))
     # keep the GPU busy a little longer so the sampler sees the load
     extra_t0 = time.time()
     while time.time() - extra_t0 < 1.0:
@@ -390,9 +427,12 @@ def run_ours(args, world, rank, local):
                    "batch_per_gpu": B, "seq_len": N, "heads": H, "head_dim": D, "model_dim": H * D,
                    "layers": layers, "parallelism": f"dp{world} (batch x head shards)",
                    "kernel_path": kernel_path(args.path, N, D, dname),
-                   "launch": "eager" if args.no_graph else ("one CUDA graph per op call, replayed back to back "
-                                                              "(events at step boundaries); per-op kernel times "
-                                                              "from a separately marked pass"),
+                   "launch": "eager" if args.no_graph else (
+                       ("one CUDA graph per step (the 2 x layers op calls; programmatic-dependent-launch "
+                        "edges between the kernels)" if args.graph_scope == "step" else
+                        "one CUDA graph per op call, replayed back to back")
+                       + " (events at step boundaries); per-op kernel times from a separately marked "
+                         "pass of per-op graphs"),
                    "l2": "flushed between timed steps (256 MiB write), outside the events"},
         "roofline": {"bound": "hbm", "kernel": "cos_bwd (backward, dominant)",
                      "achieved": bwd_gbs, "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak,
@@ -403,6 +443,7 @@ def run_ours(args, world, rank, local):
                     "bwd_us": bwd_avg * 1e6, "bwd_GBps": bwd_gbs, "bwd_frac": bwd_gbs / peak,
                     "step_GBps": step_gbs, "step_frac": step_gbs / peak},
         "gpu_launches": gpu_launches,
+        "graph_outputs_equal_eager": graph_check,
         "clocks": clocks,
     }
     if D != 32 or dname == "bf16":  # FP32-pipe kernels: compute at peak bounds them, not HBM (north star: max of both)
@@ -591,6 +632,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ml1m", choices=sorted(WORKLOADS))
+    ap.add_argument("--graph-scope", default="step", choices=["step", "op"],
+                    help="graph mode: one graph for the whole step (default) or one per op call")
     ap.add_argument("--path", default="tcgen05", choices=["tcgen05", "fp32pipe"],
                     help="d_h=32 kernels: tcgen05 3xTF32 (default) or the FP32-pipe variant")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
