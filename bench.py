@@ -81,6 +81,33 @@ def algorithmic_bytes(B, H, N, D, elt=4):
 FP32_PEAK_FLOPS = 148 * 128 * 2 * 1.965e9
 
 
+def _inputs():
+    """paper_2602_06935_b200/inputs.py loaded BY PATH: it only needs numpy
+    (and torch for device generation), and importing the package would map
+    libcotten.so into the reference arm's process."""
+    import importlib.util
+    name = "_cotten_inputs"
+    if name in sys.modules:
+        return sys.modules[name]
+    path = os.path.join(ROOT, "paper_2602_06935_b200", "inputs.py")
+    spec = importlib.util.spec_from_file_location(name, path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def workload_config(name, world):
+    """The `config` dict, identical in both arms (--impl ours / reference)."""
+    total_b, N, H, D, layers, strong, desc = WORKLOADS[name]
+    global_b = total_b if strong else total_b * world
+    return {"workload": desc, "name": name, "global_batch": global_b,
+            "batch_per_gpu": (total_b + world - 1) // world if strong else total_b,
+            "seq_len": N, "heads": H, "head_dim": D, "model_dim": H * D, "layers": layers,
+            "dtype": WORKLOAD_DTYPE.get(name, "f32"),
+            "parallelism": f"dp{world} (contiguous batch x head shards, no data-path collective)"}
+
+
 def pipe_flops(B, H, N, D):
     """SURVEY §8d flops per launch: fwd 4·N·d² + 7·N·d, bwd 8·N·d² + 12·N·d per unit."""
     return B * H * (4 * N * D * D + 7 * N * D), B * H * (8 * N * D * D + 12 * N * D)
@@ -161,7 +188,8 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def dist_setup(want_gpus):
+def dist_setup():
+    """One process per GPU (torchrun env: RANK / LOCAL_RANK / WORLD_SIZE)."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -177,6 +205,21 @@ def dist_setup(want_gpus):
     return world, rank, local
 
 
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run
+    with N local ranks (one process per GPU), so a scaling run can never
+    silently measure one GPU.  Returns the child's exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, COTTEN_BENCH_CHILD="1")
+    return subprocess.call(cmd, env=env)
+
+
 def shard(total, rank, world):
     """Contiguous batch shard [lo, hi) of rank: no collective."""
     per, rem = divmod(total, world)
@@ -189,7 +232,8 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -202,9 +246,10 @@ def barrier(world):
 
 # ---------------------------------------------------------------------------
 
-def run_ours(args, world, rank, local):
+def run_ours(args, world, rank, local, with_cpu=True):
     import torch
-    from paper_2602_06935_b200 import _lib, inputs, ops
+    from paper_2602_06935_b200 import _lib, ops
+    inputs = _inputs()
 
     total_b, N, H, D, layers, strong, desc = WORKLOADS[args.workload]
     dname = WORKLOAD_DTYPE.get(args.workload, "f32")
@@ -218,7 +263,7 @@ def run_ours(args, world, rank, local):
     # Inputs resident in HBM before the timed region (distinct per layer / rank).
     L = []
     for layer in range(layers):
-        t = inputs.make_device(B, H, N, D, seed=1000 * layer + rank, dtype=tdtype, device=dev)
+        t = inputs.make_device(B, H, N, D, seed=1000 * layer + rank + lo, dtype=tdtype, device=dev)
         valid = torch.from_numpy(inputs.left_padded_mask(B, N, 1000 * layer + rank)).to(dev)
         t.update(valid=valid,
                  out=torch.empty_like(t["q"]), S=torch.empty(B * H, D, D, device=dev),
@@ -230,163 +275,124 @@ def run_ours(args, world, rank, local):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     m = 1.0
     flags = _lib.FLAG_FP32_PIPE if args.path == "fp32pipe" else 0
-
     launches = [0]
 
-    def fwd(t):
+    def fwd(t, s):
         ops.forward(t["q"], t["k"], t["v"], t["valid"], m, out=t["out"], saved_S=t["S"],
-                    stream=stream, flags=flags)
+                    stream=s, flags=flags)
         launches[0] += _lib.launches()
 
-    def bwd(t, i):
+    def bwd(t, i, s):
         ops.backward(t["q"], t["k"], t["v"], t["valid"], m, t["d_out"], t["S"], t["dq"],
-                     t["dk"], t["dv"], t["dm_unit"], dm_tot[i:i + 1], stream=stream, flags=flags)
+                     t["dk"], t["dv"], t["dm_unit"], dm_tot[i:i + 1], stream=s, flags=flags)
         launches[0] += _lib.launches()
 
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     n_marks = 2 * layers + 1
-    args.no_graph = args.graph == "off"
 
-    def step(marks=None):
+    def step(s, marks=None):
+        """fwd of every layer, then bwd in reverse; marks[i] recorded after op i."""
         if marks is not None:
-            marks[0].record(stream)
+            marks[0].record(s)
         for i in range(layers):
-            fwd(L[i])
+            fwd(L[i], s)
             if marks is not None:
-                marks[1 + i].record(stream)
+                marks[1 + i].record(s)
         for j, i in enumerate(reversed(range(layers))):
-            bwd(L[i], i)
+            bwd(L[i], i, s)
             if marks is not None:
-                marks[1 + layers + j].record(stream)
+                marks[1 + layers + j].record(s)
+
+    def allreduce_dm():
         if world > 1:  # the op's parameter-gradient exchange (dm per layer)
             import torch.distributed as dist
             dist.all_reduce(dm_tot)
 
-    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
-        step()
+    for _ in range(max(args.warmup, 3)):
+        step(stream)
+        allreduce_dm()
     torch.cuda.synchronize()
-    # graphs only where host launch overhead paces the step (short steps); long
-    # steps measured ~4 % faster issued eagerly (ML-20M), so they stay eager
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     w0, w1 = ev(), ev()
     w0.record(stream)
-    step()
+    step(stream)
     w1.record(stream)
     torch.cuda.synchronize()
     eager_step_ms = w0.elapsed_time(w1)
-    if args.graph == "on" or (args.graph == "auto" and eager_step_ms < 2.0):
-        args.no_graph = False
-    else:
-        args.no_graph = True
+    # Graphs only where host launch overhead paces the step (short steps);
+    # long steps measured ~4 % faster issued eagerly (ML-20M), so they stay eager.
+    use_graph = args.graph == "on" or (args.graph == "auto" and eager_step_ms < 2.0)
 
-    if not args.no_graph:
-        # One CUDA graph per op call (the tensor maps, scale constants and
-        # launch geometry are baked in at capture): a replay is a single
-        # cudaGraphLaunch, so the host no longer paces small batches.  Warm-up
-        # above already allocated every workspace the calls need.
-        graphs = {}
-        counts = {}
+    gstep, gmarks = None, None
+    if use_graph:
+        # The whole step as ONE CUDA graph (inside a graph each kernel's
+        # programmatic-dependent-launch attribute becomes a programmatic edge),
+        # with external event-record nodes between the ops: the per-op kernel
+        # times behind `roofline` come from the very replays that are timed.
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
-        for i in range(layers):
-            for kind in ("fwd", "bwd"):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=cap):
-                    s_cap = torch.cuda.current_stream()
-                    if kind == "fwd":
-                        ops.forward(L[i]["q"], L[i]["k"], L[i]["v"], L[i]["valid"], m,
-                                    out=L[i]["out"], saved_S=L[i]["S"], stream=s_cap, flags=flags)
-                    else:
-                        t = L[i]
-                        ops.backward(t["q"], t["k"], t["v"], t["valid"], m, t["d_out"], t["S"],
-                                     t["dq"], t["dk"], t["dv"], t["dm_unit"], dm_tot[i:i + 1],
-                                     stream=s_cap, flags=flags)
-                    counts[(kind, i)] = _lib.launches()
-                graphs[(kind, i)] = g
-        stream.wait_stream(cap)
-        torch.cuda.synchronize()
-
-        fwd_eager, bwd_eager = fwd, bwd
-
-        def fwd(t, _i=None):  # noqa: F811
-            i = next(k for k in range(layers) if L[k] is t)
-            graphs[("fwd", i)].replay()
-            launches[0] += counts[("fwd", i)]
-
-        def bwd(t, i):  # noqa: F811
-            graphs[("bwd", i)].replay()
-            launches[0] += counts[("bwd", i)]
-
-        step_launches = sum(counts.values())
-        # The whole step as one graph too: inside a graph the kernels'
-        # programmatic-dependent-launch attribute becomes a programmatic edge,
-        # so each kernel's prologue overlaps the previous kernel's tail, which
-        # separate graph launches cannot do.
-        gstep = None
-        if args.graph_scope == "step":
-            gstep = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gstep, stream=cap):
-                s_cap = torch.cuda.current_stream()
-                for i in range(layers):
-                    t = L[i]
-                    ops.forward(t["q"], t["k"], t["v"], t["valid"], m, out=t["out"], saved_S=t["S"],
-                                stream=s_cap, flags=flags)
-                for i in reversed(range(layers)):
-                    t = L[i]
-                    ops.backward(t["q"], t["k"], t["v"], t["valid"], m, t["d_out"], t["S"], t["dq"],
-                                 t["dk"], t["dv"], t["dm_unit"], dm_tot[i:i + 1], stream=s_cap,
-                                 flags=flags)
+        with torch.cuda.stream(cap):
+            step(cap)  # first use of the capture stream: its per-stream workspace
+        cap.synchronize()
+        gmarks = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(n_marks)]
+        gstep = torch.cuda.CUDAGraph()
+        launches[0] = 0
+        with torch.cuda.graph(gstep, stream=cap):
+            step(torch.cuda.current_stream(), gmarks if args.graph_events else None)
+        step_launches = launches[0]
         stream.wait_stream(cap)
         torch.cuda.synchronize()
         for _ in range(2):
-            step()
+            gstep.replay()
         torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.25)
-    all_marks = [[ev() for _ in range(n_marks)] for _ in range(args.steps)]
-    if not args.no_graph:
-        # per-op kernel times (roofline fields) from a separately marked pass
-        for s_ in range(args.steps):
-            flush.zero_()
-            step(all_marks[s_])
-        torch.cuda.synchronize()
-        step_marks = [(ev(), ev()) for _ in range(args.steps)]
     barrier(world)
     torch.cuda.synchronize()
     launches[0] = 0
+    step_ms, op_ms = [], []
+    eager_marks = [[ev() for _ in range(n_marks)] for _ in range(args.steps)]
     for s_ in range(args.steps):
         flush.zero_()  # L2 flush between timed steps, outside the events
-        if args.no_graph:
-            step(all_marks[s_])
-        else:
-            # the step's per-op graphs back to back, events at the step boundaries only
-            step_marks[s_][0].record(stream)
-            if gstep is not None:
+        if use_graph:
+            if args.graph_events:
                 gstep.replay()
+                allreduce_dm()
+                torch.cuda.synchronize()  # read this replay's event nodes (outside the span)
+                mk = gmarks
             else:
-                for i in range(layers):
-                    graphs[("fwd", i)].replay()
-                for i in reversed(range(layers)):
-                    graphs[("bwd", i)].replay()
+                mk = eager_marks[s_]
+                mk[0].record(stream)
+                gstep.replay()
+                mk[-1].record(stream)
+                allreduce_dm()
             launches[0] += step_launches
-            if world > 1:
-                import torch.distributed as dist
-                dist.all_reduce(dm_tot)
-            step_marks[s_][1].record(stream)
+        else:
+            mk = eager_marks[s_]
+            step(stream, mk)
+            allreduce_dm()
+            if world == 1:
+                continue
+        if use_graph and not args.graph_events:
+            continue
+        step_ms.append(mk[0].elapsed_time(mk[-1]))
+        op_ms.append([mk[i].elapsed_time(mk[i + 1]) for i in range(n_marks - 1)])
     torch.cuda.synchronize()
+    if not step_ms:  # eager (world 1) / graph without event nodes: read after the loop
+        for mk in eager_marks:
+            step_ms.append(mk[0].elapsed_time(mk[-1]))
+            if not use_graph:
+                op_ms.append([mk[i].elapsed_time(mk[i + 1]) for i in range(n_marks - 1)])
     barrier(world)
     gpu_launches = launches[0]
     graph_check = None
-    if not args.no_graph:
-        # the graphs' outputs of the last timed step == a plain eager step's (same inputs)
+    if use_graph:
+        # the graph's outputs of the last timed step == a plain eager step's (same inputs)
         names = ("out", "dq", "dk", "dv")
         snap = [L[i][n].clone() for i in range(layers) for n in names]
         snap_dm = dm_tot.clone()
-        for i in range(layers):
-            fwd_eager(L[i])
-        for i in reversed(range(layers)):
-            bwd_eager(L[i], i)
+        step(stream)
         torch.cuda.synchronize()
         graph_check = all(torch.equal(a, L[i][n]) for a, (i, n) in
                           zip(snap, [(i, n) for i in range(layers) for n in names]))
@@ -395,105 +401,94 @@ def run_ours(args, world, rank, local):
     extra_t0 = time.time()
     while time.time() - extra_t0 < 1.0:
         flush.zero_()
-        step()
+        step(stream)
     torch.cuda.synchronize()
     clocks = sampler.stop()
 
-    if args.no_graph:
-        step_ms = [m_[0].elapsed_time(m_[-1]) for m_ in all_marks]
-    else:
-        step_ms = [a.elapsed_time(b) for a, b in step_marks]
-    fwd_ms = [m_[i].elapsed_time(m_[i + 1]) for m_ in all_marks for i in range(layers)]
-    bwd_ms = [m_[layers + i].elapsed_time(m_[layers + i + 1]) for m_ in all_marks
-              for i in range(layers)]
     total_ms = max_over_ranks(sum(step_ms), world)
     ms_per_step = total_ms / args.steps
     value = global_b * args.steps / (total_ms / 1e3)
 
     fwd_bytes, bwd_bytes = algorithmic_bytes(B, H, N, D, elt=2 if dname == "bf16" else 4)
     peak, peak_src = load_peaks()
-    fwd_avg = statistics.mean(fwd_ms) / 1e3
-    bwd_avg = statistics.mean(bwd_ms) / 1e3
-    bwd_gbs = bwd_bytes / bwd_avg / 1e9
-    fwd_gbs = fwd_bytes / fwd_avg / 1e9
-    step_gbs = layers * (fwd_bytes + bwd_bytes) / (ms_per_step / 1e3) / 1e9
-
     res = {
         "metric": METRIC, "value": value, "unit": "seq/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": dname,
         "data": "synthetic U(-1,1) (mix_seed per shape, bench.cpp:21-26,50), left-padded masks",
-        "config": {"workload": desc, "name": args.workload, "global_batch": global_b,
-                   "batch_per_gpu": B, "seq_len": N, "heads": H, "head_dim": D, "model_dim": H * D,
-                   "layers": layers, "parallelism": f"dp{world} (batch x head shards)",
-                   "kernel_path": kernel_path(args.path, N, D, dname),
-                   "launch": "eager" if args.no_graph else (
-                       ("one CUDA graph per step (the 2 x layers op calls; programmatic-dependent-launch "
-                        "edges between the kernels)" if args.graph_scope == "step" else
-                        "one CUDA graph per op call, replayed back to back")
-                       + " (events at step boundaries); per-op kernel times from a separately marked "
-                         "pass of per-op graphs"),
-                   "l2": "flushed between timed steps (256 MiB write), outside the events"},
-        "roofline": {"bound": "hbm", "kernel": "cos_bwd (backward, dominant)",
-                     "achieved": bwd_gbs, "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak,
-                     "traffic": None, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bwd_bytes,
-                     "avg_launch_us": bwd_avg * 1e6},
-        "kernels": {"fwd_us": fwd_avg * 1e6, "fwd_GBps": fwd_gbs, "fwd_frac": fwd_gbs / peak,
-                    "bwd_us": bwd_avg * 1e6, "bwd_GBps": bwd_gbs, "bwd_frac": bwd_gbs / peak,
-                    "step_GBps": step_gbs, "step_frac": step_gbs / peak},
+        "config": workload_config(args.workload, world),
+        "run": {"kernel_path": kernel_path(args.path, N, D, dname),
+                "shard": [lo, hi],
+                "launch": ("eager" if not use_graph else
+                           "one CUDA graph per step (programmatic-dependent-launch edges between "
+                           "the kernels" + (", external event-record nodes between the ops)"
+                                            if args.graph_events else ")")),
+                "l2": "flushed between timed steps (256 MiB write), outside the events"},
         "gpu_launches": gpu_launches,
         "graph_outputs_equal_eager": graph_check,
         "clocks": clocks,
     }
-    if D != 32 or dname == "bf16":  # FP32-pipe kernels: compute at peak bounds them, not HBM (north star: max of both)
-        ff, fb = pipe_flops(B, H, N, D)
-        t_f = max(ff / FP32_PEAK_FLOPS, fwd_bytes / (peak * 1e9))
-        t_b = max(fb / FP32_PEAK_FLOPS, bwd_bytes / (peak * 1e9))
-        res["roofline_max"] = {
-            "model": "max(compute-at-peak, bytes-at-HBM) per launch; FP32 pipe peak = 148 SM x 128 FFMA "
-                     "x 2 x 1.965 GHz (derived, no measured FP32 peak in MEASURED_PEAKS.json)",
-            "pipe": "fp32", "peak_tflops": FP32_PEAK_FLOPS / 1e12,
-            "fwd_bound": "fp32" if ff / FP32_PEAK_FLOPS > fwd_bytes / (peak * 1e9) else "hbm",
-            "bwd_bound": "fp32" if fb / FP32_PEAK_FLOPS > bwd_bytes / (peak * 1e9) else "hbm",
-            "fwd_tflops": ff / fwd_avg / 1e12, "bwd_tflops": fb / bwd_avg / 1e12,
-            "fwd_frac": t_f / fwd_avg, "bwd_frac": t_b / bwd_avg,
-            "step_frac": layers * (t_f + t_b) / (ms_per_step / 1e3)}
-    traffic = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(traffic):
-        try:
-            with open(traffic) as f:
-                tr = json.load(f).get(args.workload)
-            if tr:
-                res["roofline"]["traffic"] = tr.get("bwd")
-                res["roofline"]["traffic_source"] = "profiles/traffic.json (ncu, per launch)"
-        except Exception:
-            pass
+    if op_ms:
+        fwd_avg = statistics.mean(o[i] for o in op_ms for i in range(layers)) / 1e3
+        bwd_avg = statistics.mean(o[layers + i] for o in op_ms for i in range(layers)) / 1e3
+        bwd_gbs = bwd_bytes / bwd_avg / 1e9
+        fwd_gbs = fwd_bytes / fwd_avg / 1e9
+        step_gbs = layers * (fwd_bytes + bwd_bytes) / (ms_per_step / 1e3) / 1e9
+        res["roofline"] = {
+            "bound": "hbm", "kernel": "cos_bwd (backward, dominant)", "achieved": bwd_gbs,
+            "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak, "traffic": None,
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": bwd_bytes,
+            "avg_launch_us": bwd_avg * 1e6,
+            "timing": "CUDA events between the ops of the timed steps themselves"}
+        res["kernels"] = {"fwd_us": fwd_avg * 1e6, "fwd_GBps": fwd_gbs, "fwd_frac": fwd_gbs / peak,
+                          "bwd_us": bwd_avg * 1e6, "bwd_GBps": bwd_gbs, "bwd_frac": bwd_gbs / peak,
+                          "step_GBps": step_gbs, "step_frac": step_gbs / peak}
+        if D != 32 or dname == "bf16":  # north star: max(compute-at-peak, bytes-at-HBM)
+            ff, fb = pipe_flops(B, H, N, D)
+            t_f = max(ff / FP32_PEAK_FLOPS, fwd_bytes / (peak * 1e9))
+            t_b = max(fb / FP32_PEAK_FLOPS, bwd_bytes / (peak * 1e9))
+            res["roofline_max"] = {
+                "model": "max(compute-at-peak, bytes-at-HBM) per launch; compute = the FP32 pipe "
+                         "(148 SM x 128 FFMA x 2 x 1.965 GHz, derived); a kernel on the tensor "
+                         "pipe is bounded by HBM alone",
+                "pipe": "fp32", "peak_tflops": FP32_PEAK_FLOPS / 1e12,
+                "fwd_tflops": ff / fwd_avg / 1e12, "bwd_tflops": fb / bwd_avg / 1e12,
+                "fwd_frac": t_f / fwd_avg, "bwd_frac": t_b / bwd_avg,
+                "step_frac": layers * (t_f + t_b) / (ms_per_step / 1e3)}
+        traffic = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(traffic):
+            try:
+                with open(traffic) as f:
+                    tr = json.load(f).get(args.workload)
+                if tr:
+                    res["roofline"]["traffic"] = tr.get("bwd")
+                    res["roofline"]["traffic_source"] = "profiles/traffic.json (ncu --set full, per launch)"
+            except Exception:
+                pass
 
-    if not args.no_e2e and dname == "bf16":
-        res["e2e"] = {"value": None, "note": "bf16 points are device-resident kernel measurements only"}
-    elif not args.no_e2e:
-        res["e2e"] = run_e2e(args, world, B, N, H, D, layers, global_b)
-    if rank == 0 and world == 1 and not args.no_cpu and dname == "f32":
-        res["cpu_baseline"] = run_cpu_baseline(args, N, H, D, layers, B)
+    if not args.no_e2e:
+        res["e2e"] = run_e2e(args, world, B, N, H, D, layers, global_b, dname)
+    if with_cpu and rank == 0 and world == 1 and not args.no_cpu:
+        res["cpu_baseline"] = run_cpu_baseline(args.workload, args.cpu_seconds)
     return res
 
 
-def run_e2e(args, world, B, N, H, D, layers, global_b):
+def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
     """Same metric through the reference-facing host entry points
     (cotten_fwd_host / cotten_bwd_host: the calls under cosine_attention_fused /
     cosine_attention_backward), pinned host buffers, copies inside the timing."""
     import torch
-    from paper_2602_06935_b200 import inputs
     from paper_2602_06935_b200 import _lib
     import ctypes
+    inputs = _inputs()
 
     lib = _lib.load()
-    desc = _lib.make_desc(B, H, N, D, "f32", 1e-6)
-    p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    desc = _lib.make_desc(B, H, N, D, dname, 1e-6)
+    tdt = torch.bfloat16 if dname == "bf16" else torch.float32
+    p = lambda a: ctypes.c_void_p(a.data_ptr())  # noqa: E731
 
-    def pinned(shape, dtype=torch.float32):
-        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+    def pinned(shape, dtype=tdt):
+        return torch.empty(shape, dtype=dtype, pin_memory=True)
 
     Ls = []
     for layer in range(layers):
@@ -501,12 +496,12 @@ def run_e2e(args, world, B, N, H, D, layers, global_b):
         t = {}
         for n, x in h.items():
             t[n] = pinned(x.shape)
-            t[n][...] = x
+            t[n].copy_(torch.from_numpy(x))
         t["valid"] = pinned((B, N), torch.uint8)
-        t["valid"][...] = inputs.left_padded_mask(B, N, 7 + layer)
+        t["valid"].copy_(torch.from_numpy(inputs.left_padded_mask(B, N, 7 + layer)))
         for n in ("out", "dq", "dk", "dv"):
             t[n] = pinned((B, H, N, D))
-        t["S"] = pinned((B * H, D, D))
+        t["S"] = pinned((B * H, D, D), torch.float32)
         t["dm"] = pinned((1,), torch.float64)
         Ls.append(t)
 
@@ -526,103 +521,140 @@ def run_e2e(args, world, B, N, H, D, layers, global_b):
     for _ in range(args.steps):
         step()
     el = max_over_ranks(time.perf_counter() - t0, world)
-    tb = B * H * N * D * 4
-    h2d = layers * (3 * tb + B * N) + layers * (4 * tb + B * N + B * H * D * D * 4)
-    d2h = layers * (tb + B * H * D * D * 4) + layers * (3 * tb + 8)
+    es = 2 if dname == "bf16" else 4
+    tb = B * H * N * D * es
+    sb = B * H * D * D * 4
+    h2d = layers * (3 * tb + B * N) + layers * (4 * tb + B * N + sb)
+    d2h = layers * (tb + sb) + layers * (3 * tb + 8)
     return {"value": global_b * args.steps / el, "unit": "seq/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
-            "path": "cotten_fwd_host + cotten_bwd_host per layer (pinned host buffers)"}
+            "path": "cotten_fwd_host + cotten_bwd_host per layer (pinned host buffers, "
+                    "host wall clock around the synchronous calls)"}
 
 
-def run_cpu_baseline(args, N, H, D, layers, B, budget_s=None):
-    """The reference operator (oracle/_ref, compiled from /root/reference
-    sources) on this host's cores: the same per-layer fwd(+cache)+bwd calls
-    per (seq, head) on a persistent pool, on the same shape."""
-    import oracle
-    from paper_2602_06935_b200 import inputs
-    budget_s = args.cpu_seconds if budget_s is None else budget_s
-    threads = os.cpu_count() or 1
-    if not oracle.ref_available():
-        return {"value": None, "unit": "seq/s", "cores": threads, "kind": "reference",
-                "sample": "unavailable: oracle/_ref/libcosrec_ref.so not built"}
-    Bs = min(B, 256)
-    per_layer = []
-    for layer in range(layers):
-        h = inputs.make_host(Bs, H, N, D, seed=7 + layer)
-        valid = inputs.left_padded_mask(Bs, N, 7 + layer)
-        outs = tuple(np.empty(h["q"].shape, np.float32) for _ in range(4)) + (np.zeros(Bs * H),)
-        per_layer.append((h, valid, outs))
-
-    def one():
-        for h, valid, outs in per_layer:
-            oracle.ref_batched_f32(h["q"], h["k"], h["v"], h["d_out"], valid, 1.0, 1e-6,
-                                   threads, outs)
-
-    one()  # warm-up (pool spawn, first touch)
-    times = []
-    t_start = time.perf_counter()
-    while time.perf_counter() - t_start < budget_s or len(times) < 3:
-        t0 = time.perf_counter()
-        one()
-        times.append(time.perf_counter() - t0)
-    med = statistics.median(times)
-    cpu = ""
-    try:
-        with open("/proc/cpuinfo") as f:
-            cpu = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
-    except Exception:
-        pass
-    return {"value": Bs / med, "unit": "seq/s", "cores": threads, "kind": "reference",
-            "sample": f"{Bs} sequences x {layers} layer(s) of cosine_attention_fused(+cache,+mask)"
-                      f" + cosine_attention_backward per (seq, head), median of {len(times)} reps"
-                      f" over {time.perf_counter() - t_start:.1f}s, {threads} threads, {cpu}"}
+# Core-seconds per sequence per (head * N * d_h^2) of the reference operator
+# (fwd + cache + bwd), measured on the ML-1M shape; only sizes the CPU sample.
+_CPU_COST = 5e-9
 
 
-def run_reference(args, world, rank):
-    """--impl reference: the reference's own CPU operator on this host."""
-    if rank != 0:
-        return None
-    total_b, N, H, D, layers, strong, desc = WORKLOADS[args.workload]
-    import oracle
-    from paper_2602_06935_b200 import inputs
-    threads = os.cpu_count() or 1
-    Bs = min(total_b, 256)
+def cpu_sample_size(workload, threads, seconds_per_rep=1.0):
+    total_b, N, H, D, layers, strong, desc = WORKLOADS[workload]
+    per_seq = _CPU_COST * H * N * D * D * layers
+    bs = int(seconds_per_rep * threads / per_seq)
+    bs = max(threads, (bs // threads) * threads)
+    return min(total_b, bs, 4096)
+
+
+def _cpu_sample(workload, threads):
+    """A bounded, seeded sample of the workload on the host (f32 inputs; the
+    reference computes in f64 on them)."""
+    inputs = _inputs()
+    total_b, N, H, D, layers, strong, desc = WORKLOADS[workload]
+    Bs = cpu_sample_size(workload, threads)
     data = []
     for layer in range(layers):
         h = inputs.make_host(Bs, H, N, D, seed=7 + layer)
         valid = inputs.left_padded_mask(Bs, N, 7 + layer)
         outs = tuple(np.empty(h["q"].shape, np.float32) for _ in range(4)) + (np.zeros(Bs * H),)
         data.append((h, valid, outs))
+    return Bs, data
 
-    def step():
-        for h, valid, outs in data:
-            oracle.ref_batched_f32(h["q"], h["k"], h["v"], h["d_out"], valid, 1.0, 1e-6,
-                                   threads, outs)
 
+def _cpu_step(data, threads):
+    import oracle
+    for h, valid, outs in data:
+        oracle.ref_batched_f32(h["q"], h["k"], h["v"], h["d_out"], valid, 1.0, 1e-6, threads, outs,
+                               release=True)
+
+
+def _cpu_desc():
+    try:
+        with open("/proc/cpuinfo") as f:
+            return next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except Exception:
+        return ""
+
+
+def run_cpu_baseline(workload, budget_s=10.0):
+    """The reference operator (oracle/_ref, compiled from /root/reference
+    sources with its stock Release flags) on this host's cores: per layer,
+    cosine_attention_fused(+cache, +mask) then cosine_attention_backward per
+    (sequence, head) on a persistent pool, over a bounded sample."""
+    import oracle
+    threads = os.cpu_count() or 1
+    if not oracle.ref_available(release=True):
+        return {"value": None, "unit": "seq/s", "cores": threads, "kind": "reference",
+                "sample": "unavailable: oracle/_ref/libcosrec_ref_release.so not built"}
+    Bs, data = _cpu_sample(workload, threads)
+    _cpu_step(data, threads)  # warm-up (pool spawn, first touch)
+    times = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s or len(times) < 3:
+        t0 = time.perf_counter()
+        _cpu_step(data, threads)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    total_b, N, H, D, layers = WORKLOADS[workload][:5]
+    return {"value": Bs / med, "unit": "seq/s", "cores": threads, "kind": "reference",
+            "sample": f"{Bs} of the {total_b} sequences x {layers} layer(s) of "
+                      f"cosine_attention_fused(+cache,+mask) + cosine_attention_backward per "
+                      f"(seq, head), reference built -O3 -DNDEBUG (its Release flags), median of "
+                      f"{len(times)} reps over {time.perf_counter() - t_start:.1f}s, {threads} "
+                      f"threads, {_cpu_desc()}"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's own CPU operator on this host (rank 0
+    only), on a bounded sample of the same workload per step.  Nothing of the
+    product package is imported or loaded here."""
+    if rank != 0:
+        return None
+    import oracle
+    total_b, N, H, D, layers, strong, desc = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    if not oracle.ref_available(release=True):
+        return {"impl": "reference", "unavailable": "oracle/_ref/libcosrec_ref_release.so not built"}
+    Bs, data = _cpu_sample(args.workload, threads)
     for _ in range(max(args.warmup, 1)):
-        step()
+        _cpu_step(data, threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        step()
+        _cpu_step(data, threads)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = Bs * args.steps / total
+    gb = workload_config(args.workload, world)["global_batch"]
     sample = (f"{Bs}-sequence sample of the {total_b}-sequence batch per step" if Bs < total_b
               else f"full {Bs}-sequence batch per step") + \
-        f", {layers} layer(s), reference operator (oracle/_ref), {threads} threads"
+        f", {layers} layer(s), reference operator (oracle/_ref, -O3 -DNDEBUG), {threads} threads"
     return {"metric": METRIC, "value": value, "unit": "seq/s", "impl": "reference",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total / args.steps * 1e3 * (total_b / Bs if strong else 1.0),
-            "higher_is_better": True, "scaling": "strong" if strong else "weak",
-            "vs_baseline": None, "dtype": "f64 (reference arithmetic; f32 inputs)",
-            "data": "synthetic", "config": {"workload": desc, "name": args.workload,
-                                            "global_batch": total_b, "seq_len": N, "heads": H,
-                                            "head_dim": D, "layers": layers},
+            "ms_per_step": gb / value * 1e3, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": "f64 (reference arithmetic; f32 inputs)", "data": "synthetic",
+            "config": workload_config(args.workload, world),
             "cpu_baseline": {"value": value, "unit": "seq/s", "cores": threads,
                              "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": "seq/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+def run_plan(args, world, rank):
+    """--plan: the launcher / sharding / config path without touching a GPU
+    (each rank reports its shard; rank 0 prints the line)."""
+    total_b, N, H, D, layers, strong, desc = WORKLOADS[args.workload]
+    lo, hi = shard(total_b, rank, world) if strong else (0, total_b)
+    shards = [[lo, hi]]
+    if world > 1:
+        import torch.distributed as dist
+        allsh = [None] * world
+        dist.all_gather_object(allsh, [lo, hi])
+        shards = allsh
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "value": None, "unit": "seq/s", "n_gpus": world, "plan": True,
+            "config": workload_config(args.workload, world), "shards": shards}
 
 
 def main():
@@ -632,21 +664,26 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ml1m", choices=sorted(WORKLOADS))
-    ap.add_argument("--graph-scope", default="step", choices=["step", "op"],
-                    help="graph mode: one graph for the whole step (default) or one per op call")
     ap.add_argument("--path", default="tcgen05", choices=["tcgen05", "fp32pipe"],
                     help="d_h=32 kernels: tcgen05 3xTF32 (default) or the FP32-pipe variant")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
-                    help="replay captured CUDA graphs of the op calls (auto: when the eager step < 2 ms)")
+                    help="replay the step as one CUDA graph (auto: when the eager step < 2 ms)")
+    ap.add_argument("--no-graph-events", dest="graph_events", action="store_false",
+                    help="graph mode: no event nodes between the ops (step time only, no roofline)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-steady", action="store_true",
                     help="skip the ML-20M steady-state block appended to the default (ml1m) line")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--plan", action="store_true", help="print the shard plan only (no GPU)")
     args = ap.parse_args()
 
-    world, rank, local = dist_setup(args.gpus)
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    world, rank, local = dist_setup()
+    if args.plan:
+        res = run_plan(args, world, rank)
+    elif args.impl == "reference":
         res = run_reference(args, world, rank)
     else:
         res = run_ours(args, world, rank, local)
@@ -658,14 +695,16 @@ def main():
             import torch
             torch.cuda.empty_cache()
             a2 = copy.copy(args)
-            a2.workload, a2.steps, a2.warmup, a2.no_e2e, a2.no_cpu = "ml20m", 5, 3, True, True
-            r2 = run_ours(a2, world, rank, local)
+            a2.workload, a2.steps, a2.warmup, a2.no_e2e = "ml20m", 5, 3, True
+            r2 = run_ours(a2, world, rank, local, with_cpu=False)
             res["steady_state"] = {
                 "workload": r2["config"]["workload"], "value": r2["value"], "unit": "seq/s",
-                "ms_per_step": r2["ms_per_step"], "launch": r2["config"]["launch"],
+                "ms_per_step": r2["ms_per_step"], "launch": r2["run"]["launch"],
                 "step_frac_of_hbm": r2["kernels"]["step_frac"],
                 "fwd_frac": r2["kernels"]["fwd_frac"], "bwd_frac": r2["kernels"]["bwd_frac"],
                 "roofline": r2["roofline"], "clocks": r2["clocks"]}
+            if not args.no_cpu:
+                res["steady_state"]["cpu_baseline"] = run_cpu_baseline("ml20m", args.cpu_seconds / 2)
             torch.cuda.empty_cache()
     if rank == 0 and res is not None:
         print(json.dumps(res), flush=True)

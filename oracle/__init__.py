@@ -1,12 +1,15 @@
 """TEST INFRASTRUCTURE ONLY — ctypes loaders for the CPU checkers.
 
 Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline / --impl
-reference legs may import this package.  Two libraries:
+reference legs may import this package.  Libraries:
 
 * ``libcosine_oracle.so`` — the plain-C float64 restatement (cosine_oracle.c),
   citing /root/reference/proj/src/attention.cpp line by line;
 * ``_ref/libcosrec_ref.so`` — the unmodified reference operator compiled from
-  its own sources (oracle/Makefile) behind ref_shim.cpp's extern "C" calls.
+  its own sources (oracle/Makefile) behind ref_shim.cpp's extern "C" calls,
+  with -O2 -ffp-contract=off (the bit-exact parity pin);
+* ``_ref/libcosrec_ref_release.so`` — the same sources with the reference's
+  stock Release flags (-O3 -DNDEBUG): the timed CPU baseline.
 """
 from __future__ import annotations
 
@@ -18,10 +21,13 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "libcosine_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libcosrec_ref.so")
+# the same sources with the reference's stock Release flags (-O3 -DNDEBUG,
+# proj/CMakeLists.txt:5-7): what bench.py times as the CPU baseline
+REF_RELEASE_SO = os.path.join(HERE, "_ref", "libcosrec_ref_release.so")
 
 _vp, _sz, _i64, _dbl = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int64, ctypes.c_double
 _o = None
-_r = None
+_r = {}
 
 
 def _oracle():
@@ -41,16 +47,16 @@ def _oracle():
     return _o
 
 
-def ref_available() -> bool:
-    return os.path.exists(REF_SO)
+def ref_available(release=False) -> bool:
+    return os.path.exists(REF_RELEASE_SO if release else REF_SO)
 
 
-def _ref():
-    global _r
-    if _r is None:
-        if not ref_available():
-            raise ImportError(f"{REF_SO} missing: run `make -C oracle` where /root/reference exists")
-        lib = ctypes.CDLL(REF_SO)
+def _ref(release=False):
+    if release not in _r:
+        path = REF_RELEASE_SO if release else REF_SO
+        if not os.path.exists(path):
+            raise ImportError(f"{path} missing: run `make -C oracle` where /root/reference exists")
+        lib = ctypes.CDLL(path)
         lib.cosref_fwd.argtypes = [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _i64] + [_vp] * 7
         lib.cosref_fwd_bwd.argtypes = [_vp, _vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _i64] + [_vp] * 6
         lib.cosref_naive.argtypes = [_vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _vp]
@@ -61,8 +67,8 @@ def _ref():
         for f in ("cosref_fwd", "cosref_fwd_bwd", "cosref_naive", "cosref_bwd_without_cache",
                   "cosref_batched_f32", "cosref_hardware_threads"):
             getattr(lib, f).restype = ctypes.c_int
-        _r = lib
-    return _r
+        _r[release] = lib
+    return _r[release]
 
 
 def _p(a):
@@ -187,16 +193,18 @@ def ref_hardware_threads() -> int:
     return int(_ref().cosref_hardware_threads())
 
 
-def ref_batched_f32(q, k, v, d_out, valid, m=1.0, eps=1e-6, threads=0, outputs=None, tile=32):
+def ref_batched_f32(q, k, v, d_out, valid, m=1.0, eps=1e-6, threads=0, outputs=None, tile=32,
+                    release=False):
     """The reference operator over a contiguous float32 [B,H,N,D] batch on a
-    persistent thread pool (threads <= 0: all host threads)."""
+    persistent thread pool (threads <= 0: all host threads).  release=True
+    uses the Release-flag build (the timed CPU baseline)."""
     B, H, N, D = q.shape
     if outputs is None:
         outputs = tuple(np.empty(q.shape, np.float32) for _ in range(4)) + (np.zeros(B * H),)
     out, dq, dk, dv, dm = outputs
     vm = _mask(valid)
     msb = 0 if vm is None else vm.shape[1]
-    lib = _ref()
+    lib = _ref(release)
     _rc(lib.cosref_batched_f32(_p(q), _p(k), _p(v), _p(d_out), _p(vm), B, H, N, D, H * N * D,
                                N * D, D, msb, m, eps, tile, _p(out), _p(dq), _p(dk), _p(dv),
                                _p(dm), int(threads)), lib)

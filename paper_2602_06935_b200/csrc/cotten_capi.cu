@@ -1,5 +1,5 @@
 // C-ABI of the cosine-attention operator (include/cotten.h): validation,
-// kernel dispatch, per-thread workspaces and the host-buffer entry points.
+// kernel dispatch, per-stream workspaces and the host-buffer entry points.
 // Error conventions mirror the reference C API (capi.cpp:21-44).
 #include <cuda_runtime.h>
 
@@ -8,8 +8,10 @@
 #include <cstdio>
 #include <cstring>
 #include <type_traits>
+#include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cotten.h"
@@ -153,35 +155,58 @@ int* device_status_word() {
   return g_status[dev];
 }
 
-// Grow-only device scratch, one per (thread, device); used for per-unit dm
-// and a recomputed S when the caller passes none.  Allocation happens only
-// when a call needs more than any earlier call (never in steady state).
+// Grow-only device scratch (per-unit dm, a recomputed S, the generic
+// backward's G workspace, the tcgen05 backward's CTA-completion counter).
+// One set per (device, stream): launches on one stream are ordered, so they
+// may share it, and launches on different streams never do (two concurrent
+// cotten_bwd(..., dm_total) calls on two streams each get their own counter).
+// Allocation happens only when a call needs more than any earlier call on
+// that stream; during CUDA-graph capture it is refused (warm the stream up
+// with one eager call first, as graph capture requires anyway).
 struct Scratch {
   void* ptr = nullptr;
   size_t bytes = 0;
-  int dev = -1;
-  void* get(size_t need, bool zeroed = false) {
-    int cur = 0;
-    COTTEN_CUDA(cudaGetDevice(&cur));
-    if (dev != cur) {  // another device: drop our (stale) handle, allocate anew
-      ptr = nullptr;
-      bytes = 0;
-      dev = cur;
-    }
-    if (need > bytes) {
-      if (ptr) cudaFree(ptr);
-      ptr = nullptr;
-      COTTEN_CUDA(cudaMalloc(&ptr, need));
-      if (zeroed) COTTEN_CUDA(cudaMemset(ptr, 0, need));  // kernels keep it zero between launches
-      bytes = need;
-    }
-    return ptr;
+};
+struct StreamScratch {
+  Scratch slot[4];
+};
+enum ScratchSlot { kScrDm, kScrS, kScrG, kScrCounter };
+struct ScratchKey {
+  int dev;
+  cudaStream_t st;
+  std::thread::id tid;  // only for the per-thread default stream
+  bool operator<(const ScratchKey& o) const {
+    if (dev != o.dev) return dev < o.dev;
+    if (st != o.st) return st < o.st;
+    return tid < o.tid;
   }
 };
-// g_counter: the CTA-completion counter of the tcgen05 backward's in-kernel dm
-// total (per host thread, like the other scratch: calls of one thread are
-// stream-ordered by the reference's usage).
-thread_local Scratch g_dm_scratch, g_s_scratch, g_g_scratch, g_counter;
+std::mutex g_scratch_mu;
+std::map<ScratchKey, StreamScratch> g_scratch;  // entries live for the process
+
+void* scratch_get(cudaStream_t st, ScratchSlot which, size_t need, bool zeroed = false) {
+  int dev = 0;
+  COTTEN_CUDA(cudaGetDevice(&dev));
+  const ScratchKey key{dev, st,
+                       st == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id()};
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  Scratch& s = g_scratch[key].slot[which];
+  if (need > s.bytes) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      throw Error{COTTEN_ERR_INTERNAL,
+                  "cotten: workspace growth during graph capture (run one eager call on this "
+                  "stream with the same shape before capturing)"};
+    if (s.ptr) COTTEN_CUDA(cudaStreamSynchronize(st));  // earlier launches may still use it
+    if (s.ptr) cudaFree(s.ptr);
+    s.ptr = nullptr;
+    s.bytes = 0;
+    COTTEN_CUDA(cudaMalloc(&s.ptr, need));
+    if (zeroed) COTTEN_CUDA(cudaMemset(s.ptr, 0, need));  // kernels keep it zero between launches
+    s.bytes = need;
+  }
+  return s.ptr;
+}
 
 // ---- launches -------------------------------------------------------------
 
@@ -236,7 +261,7 @@ void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
       usage("cotten: head_dim " + std::to_string(L.D) + " exceeds the shared-memory budget");
     const size_t smem = gen_bwd_smem<A>(L.D, gg);
     auto kern = gg ? cos_bwd_generic<T, A, true> : cos_bwd_generic<T, A, false>;
-    if (gg) p.workspace = g_g_scratch.get(L.units() * L.D * L.D * sizeof(A));
+    if (gg) p.workspace = scratch_get(st, kScrG, L.units() * L.D * L.D * sizeof(A));
     COTTEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)L.units(), kGenThreads, smem, st>>>(p);
     g_launches += 1;
@@ -292,7 +317,7 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
   p.m = m;
   p.status = device_status_word();
   if (saved_S == nullptr) {  // recompute the state with an S-only forward
-    void* s = g_s_scratch.get(L.units() * L.D * L.D * acc_size(L.dtype));
+    void* s = scratch_get(st, kScrS, L.units() * L.D * L.D * acc_size(L.dtype));
     OpParams f = p;
     f.saved_S = s;
     launch_fwd(L, f, st);
@@ -304,13 +329,14 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
   p.dk = dk;
   p.dv = dv;
   p.dm_unit = dm_unit;
-  if (dm_total && !dm_unit) p.dm_unit = static_cast<double*>(g_dm_scratch.get(L.units() * sizeof(double)));
+  if (dm_total && !dm_unit)
+    p.dm_unit = static_cast<double*>(scratch_get(st, kScrDm, L.units() * sizeof(double)));
   const bool tc_path = L.dtype == COTTEN_F32 &&
                        !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE)) &&
                        tc_bwd_supported<float>(p);
   if (dm_total && tc_path) {  // the tcgen05 kernel's last CTA writes the total (no extra launch)
     p.dm_total = dm_total;
-    p.grid_done = static_cast<unsigned*>(g_counter.get(sizeof(unsigned), true));
+    p.grid_done = static_cast<unsigned*>(scratch_get(st, kScrCounter, sizeof(unsigned), true));
   }
   launch_bwd(L, p, st);
   if (dm_total && !tc_path) {
@@ -358,30 +384,26 @@ int max_slices() {
   return v;
 }
 
+// One staging context per (host thread, device): a thread that alternates
+// between GPUs keeps each device's buffers and streams (nothing is dropped
+// or leaked on a switch).
 struct HostCtx {
   cudaStream_t stream = nullptr;
   cudaStream_t pipe[kPipe] = {};
   int dev = -1;
-  std::vector<void*> bufs;
-  std::vector<size_t> sizes;
+  void* bufs[12] = {};
+  size_t sizes[12] = {};
   ~HostCtx() {
     // Process teardown may have destroyed the context already; ignore errors.
+    if (dev < 0 || cudaSetDevice(dev) != cudaSuccess) return;
     for (void* b : bufs)
       if (b) cudaFree(b);
     if (stream) cudaStreamDestroy(stream);
     for (cudaStream_t p : pipe)
       if (p) cudaStreamDestroy(p);
   }
-  void ensure() {
-    int cur = 0;
-    COTTEN_CUDA(cudaGetDevice(&cur));
-    if (dev != cur) {
-      bufs.assign(12, nullptr);
-      sizes.assign(12, 0);
-      stream = nullptr;
-      for (cudaStream_t& p : pipe) p = nullptr;
-      dev = cur;
-    }
+  void ensure(int cur) {
+    dev = cur;
     if (stream == nullptr) COTTEN_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     for (cudaStream_t& p : pipe)
       if (p == nullptr) COTTEN_CUDA(cudaStreamCreateWithFlags(&p, cudaStreamNonBlocking));
@@ -390,35 +412,56 @@ struct HostCtx {
     if (need > sizes[slot]) {
       if (bufs[slot]) cudaFree(bufs[slot]);
       bufs[slot] = nullptr;
+      sizes[slot] = 0;
       COTTEN_CUDA(cudaMalloc(&bufs[slot], need));
       sizes[slot] = need;
     }
     return bufs[slot];
   }
 };
-thread_local HostCtx g_host;
+thread_local std::map<int, HostCtx> g_hosts;
+thread_local HostCtx* g_host = nullptr;
+// Select (creating on first use) the calling thread's context on the current device.
+void host_begin() {
+  int cur = 0;
+  COTTEN_CUDA(cudaGetDevice(&cur));
+  g_host = &g_hosts[cur];
+  g_host->ensure(cur);
+}
 
 enum Slot { kQ, kK, kV, kO, kDO, kDQ, kDK, kDV, kMask, kS, kNorms, kDm };
 
 void* h2d(int slot, const void* src, size_t bytes) {
-  void* dst = g_host.buf(slot, bytes);
-  COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g_host.stream));
+  void* dst = g_host->buf(slot, bytes);
+  COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g_host->stream));
   return dst;
 }
 void d2h(void* dst, const void* src, size_t bytes) {
-  if (dst) COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g_host.stream));
+  if (dst) COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g_host->stream));
 }
 
-// Slices of whole sequences for the pipelined host path (f64 keeps the single
-// stream: its large-d_h backward uses a shared global workspace).
+// Slices of whole sequences for the pipelined host path.  A slice of
+// sequences is one contiguous byte range only when the batch is the outermost
+// dimension (sb * B == span); any other dense layout ([N][B][H][D],
+// [H][B][N][D], ...) is staged as one slice covering the whole span.  f64 and
+// the generic kernels' shapes stay on one slice too (their launches are
+// short and per-slice scratch would only multiply workspace).
 struct Slices {
   int64_t per = 0;  // sequences per slice
   int n = 1;
+  bool batch_major = true;
+  size_t bytes(const Layout& L, int64_t nb, size_t es) const {
+    return batch_major ? (size_t)(nb * L.sb) * es : (size_t)L.span() * es;
+  }
 };
 Slices plan_slices(const Layout& L, size_t tensor_bytes) {
   Slices sl;
+  sl.batch_major = L.sb * L.B == L.span();
   int n = (int)std::min<size_t>(max_slices(), std::max<size_t>(1, tensor_bytes / slice_bytes()));
-  if (L.dtype == COTTEN_F64) n = 1;
+  const bool fast_shape = L.D == 32 || L.D == 64 || L.D == 128;
+  if (L.dtype == COTTEN_F64 || !fast_shape || (L.flags & COTTEN_FLAG_FORCE_GENERIC) ||
+      !sl.batch_major)
+    n = 1;
   n = (int)std::min<int64_t>(n, L.B);
   sl.per = (L.B + n - 1) / n;
   sl.n = (int)((L.B + sl.per - 1) / sl.per);
@@ -431,7 +474,7 @@ void pipe_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (dst && bytes) COTTEN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
 }
 void pipe_sync() {
-  for (cudaStream_t p : g_host.pipe) COTTEN_CUDA(cudaStreamSynchronize(p));
+  for (cudaStream_t p : g_host->pipe) COTTEN_CUDA(cudaStreamSynchronize(p));
 }
 template <typename P>
 P* at(P* base, int64_t bytes) {
@@ -497,25 +540,25 @@ int cotten_fwd_host(const cotten_desc* desc, const void* q, const void* k, const
     if (!q || !k || !v) usage("cosine_attention_fused: null input");
     host_check_mask(L, valid, "cosine_attention_fused");
     L.require_dense("cosine_attention_fused");
-    g_host.ensure();
+    host_begin();
     const size_t tb = L.span() * elem_size(L.dtype);
     const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
     const size_t nbytes = L.units() * 2 * L.N * acc_size(L.dtype);
     const size_t es = elem_size(L.dtype), as = acc_size(L.dtype);
-    void* dq = g_host.buf(kQ, tb);
-    void* dk = g_host.buf(kK, tb);
-    void* dv = g_host.buf(kV, tb);
-    uint8_t* dmask = valid ? static_cast<uint8_t*>(g_host.buf(kMask, (L.B - 1) * L.msb + L.N)) : nullptr;
-    void* dout = out ? g_host.buf(kO, tb) : nullptr;
-    void* dS = saved_S ? g_host.buf(kS, sbytes) : nullptr;
-    void* dN = saved_norms ? g_host.buf(kNorms, nbytes) : nullptr;
+    void* dq = g_host->buf(kQ, tb);
+    void* dk = g_host->buf(kK, tb);
+    void* dv = g_host->buf(kV, tb);
+    uint8_t* dmask = valid ? static_cast<uint8_t*>(g_host->buf(kMask, (L.B - 1) * L.msb + L.N)) : nullptr;
+    void* dout = out ? g_host->buf(kO, tb) : nullptr;
+    void* dS = saved_S ? g_host->buf(kS, sbytes) : nullptr;
+    void* dN = saved_norms ? g_host->buf(kNorms, nbytes) : nullptr;
     const Slices sl = plan_slices(L, tb);
     for (int i = 0; i < sl.n; ++i) {  // pipelined slices of whole sequences
-      cudaStream_t st = g_host.pipe[i % kPipe];
+      cudaStream_t st = g_host->pipe[i % kPipe];
       const int64_t b0 = i * sl.per, nb = std::min(sl.per, L.B - b0);
       Layout Lc = L;
       Lc.B = nb;
-      const size_t off = b0 * L.sb * es, len = nb * L.sb * es;
+      const size_t off = b0 * L.sb * es, len = sl.bytes(L, nb, es);
       const size_t soff = b0 * L.H * L.D * L.D * as, slen = nb * L.H * L.D * L.D * as;
       const size_t noff = b0 * L.H * 2 * L.N * as, nlen = nb * L.H * 2 * L.N * as;
       pipe_h2d(at(dq, off), at(q, off), len, st);
@@ -542,27 +585,27 @@ int cotten_bwd_host(const cotten_desc* desc, const void* q, const void* k, const
     if (!dq || !dk || !dv) usage("cosine_attention_backward: null gradient output");
     host_check_mask(L, valid, "cosine_attention_backward");
     L.require_dense("cosine_attention_backward");
-    g_host.ensure();
+    host_begin();
     const size_t tb = L.span() * elem_size(L.dtype);
     const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
     const size_t es = elem_size(L.dtype), as = acc_size(L.dtype);
-    void* gq = g_host.buf(kQ, tb);
-    void* gk = g_host.buf(kK, tb);
-    void* gv = g_host.buf(kV, tb);
-    void* gdo = g_host.buf(kDO, tb);
-    uint8_t* dmask = valid ? static_cast<uint8_t*>(g_host.buf(kMask, (L.B - 1) * L.msb + L.N)) : nullptr;
-    void* gS = g_host.buf(kS, sbytes);  // uploaded, or recomputed per slice when not given
-    void* gdq = g_host.buf(kDQ, tb);
-    void* gdk = g_host.buf(kDK, tb);
-    void* gdv = g_host.buf(kDV, tb);
-    double* gdm = static_cast<double*>(g_host.buf(kDm, (L.units() + 1) * sizeof(double)));
+    void* gq = g_host->buf(kQ, tb);
+    void* gk = g_host->buf(kK, tb);
+    void* gv = g_host->buf(kV, tb);
+    void* gdo = g_host->buf(kDO, tb);
+    uint8_t* dmask = valid ? static_cast<uint8_t*>(g_host->buf(kMask, (L.B - 1) * L.msb + L.N)) : nullptr;
+    void* gS = g_host->buf(kS, sbytes);  // uploaded, or recomputed per slice when not given
+    void* gdq = g_host->buf(kDQ, tb);
+    void* gdk = g_host->buf(kDK, tb);
+    void* gdv = g_host->buf(kDV, tb);
+    double* gdm = static_cast<double*>(g_host->buf(kDm, (L.units() + 1) * sizeof(double)));
     const Slices sl = plan_slices(L, tb);
     for (int i = 0; i < sl.n; ++i) {  // pipelined slices of whole sequences
-      cudaStream_t st = g_host.pipe[i % kPipe];
+      cudaStream_t st = g_host->pipe[i % kPipe];
       const int64_t b0 = i * sl.per, nb = std::min(sl.per, L.B - b0);
       Layout Lc = L;
       Lc.B = nb;
-      const size_t off = b0 * L.sb * es, len = nb * L.sb * es;
+      const size_t off = b0 * L.sb * es, len = sl.bytes(L, nb, es);
       const size_t soff = b0 * L.H * L.D * L.D * as, slen = nb * L.H * L.D * L.D * as;
       const uint8_t* mk = dmask ? dmask + b0 * L.msb : nullptr;
       pipe_h2d(at(gq, off), at(q, off), len, st);
@@ -584,12 +627,12 @@ int cotten_bwd_host(const cotten_desc* desc, const void* q, const void* k, const
     }
     pipe_sync();
     if (dm_total) {  // the same partition and tree as the single-launch total (bit-identical)
-      dm_reduce_kernel<<<1, 256, 0, g_host.stream>>>(gdm, L.units(), gdm + L.units());
+      dm_reduce_kernel<<<1, 256, 0, g_host->stream>>>(gdm, L.units(), gdm + L.units());
       g_launches += 1;
       COTTEN_CUDA(cudaGetLastError());
       d2h(dm_total, gdm + L.units(), sizeof(double));
     }
-    COTTEN_CUDA(cudaStreamSynchronize(g_host.stream));
+    COTTEN_CUDA(cudaStreamSynchronize(g_host->stream));
   });
 }
 
@@ -603,7 +646,7 @@ int cotten_fwd_bwd_host(const cotten_desc* desc, const void* q, const void* k, c
     if (!out || !dq || !dk || !dv) usage("cosine_attention_fused: null output");
     host_check_mask(L, valid, "cosine_attention_fused");
     L.require_dense("cosine_attention_fused");
-    g_host.ensure();
+    host_begin();
     const size_t tb = L.span() * elem_size(L.dtype);
     const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
     void* gq = h2d(kQ, q, tb);
@@ -612,21 +655,21 @@ int cotten_fwd_bwd_host(const cotten_desc* desc, const void* q, const void* k, c
     void* gdo = h2d(kDO, d_out, tb);
     const uint8_t* dmask =
         valid ? static_cast<const uint8_t*>(h2d(kMask, valid, (L.B - 1) * L.msb + L.N)) : nullptr;
-    void* go = g_host.buf(kO, tb);
-    void* gS = g_host.buf(kS, sbytes);
-    void* gdq = g_host.buf(kDQ, tb);
-    void* gdk = g_host.buf(kDK, tb);
-    void* gdv = g_host.buf(kDV, tb);
-    double* gdm = static_cast<double*>(g_host.buf(kDm, (L.units() + 1) * sizeof(double)));
-    device_fwd(L, gq, gk, gv, dmask, m, go, gS, nullptr, g_host.stream);
+    void* go = g_host->buf(kO, tb);
+    void* gS = g_host->buf(kS, sbytes);
+    void* gdq = g_host->buf(kDQ, tb);
+    void* gdk = g_host->buf(kDK, tb);
+    void* gdv = g_host->buf(kDV, tb);
+    double* gdm = static_cast<double*>(g_host->buf(kDm, (L.units() + 1) * sizeof(double)));
+    device_fwd(L, gq, gk, gv, dmask, m, go, gS, nullptr, g_host->stream);
     device_bwd(L, gq, gk, gv, dmask, m, gdo, gS, gdq, gdk, gdv, gdm, gdm + L.units(),
-               g_host.stream);
+               g_host->stream);
     d2h(out, go, tb);
     d2h(dq, gdq, tb);
     d2h(dk, gdk, tb);
     d2h(dv, gdv, tb);
     d2h(dm_total, gdm + L.units(), sizeof(double));
-    COTTEN_CUDA(cudaStreamSynchronize(g_host.stream));
+    COTTEN_CUDA(cudaStreamSynchronize(g_host->stream));
   });
 }
 

@@ -250,6 +250,14 @@ def _same_layout(ref, *ts):
             raise ShapeError("shape mismatch: all operands must share shape, strides and dtype")
 
 
+def _like(t):
+    """An output with t's shape AND strides (storage covering t's span): the
+    kernels write outputs at the inputs' strides, so a gapped q (a slice of a
+    fused QKV projection) needs a gapped output, not empty_like's dense one."""
+    import torch
+    return torch.empty_strided(t.size(), t.stride(), dtype=t.dtype, device=t.device)
+
+
 def _tp(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
@@ -267,7 +275,7 @@ def forward(q, k, v, valid=None, m=1.0, eps=1e-6, out=None, saved_S=None, saved_
     _same_layout(q, k, v, out)
     desc = _tdesc(q, eps, flags, valid)
     if out is None:
-        out = torch.empty_like(q)
+        out = _like(q)
     check(load().cotten_fwd(ctypes.byref(desc), _tp(q), _tp(k), _tp(v), _tp(valid), float(m),
                             _tp(out), _tp(saved_S), _tp(saved_norms), _stream(stream)))
     return out
@@ -279,9 +287,9 @@ def backward(q, k, v, valid, m, d_out, saved_S, dq=None, dk=None, dv=None, dm_un
     import torch
     _same_layout(q, k, v, d_out, dq, dk, dv)
     desc = _tdesc(q, eps, flags, valid)
-    dq = torch.empty_like(q) if dq is None else dq
-    dk = torch.empty_like(q) if dk is None else dk
-    dv = torch.empty_like(q) if dv is None else dv
+    dq = _like(q) if dq is None else dq
+    dk = _like(q) if dk is None else dk
+    dv = _like(q) if dv is None else dv
     check(load().cotten_bwd(ctypes.byref(desc), _tp(q), _tp(k), _tp(v), _tp(valid), float(m),
                             _tp(d_out), _tp(saved_S), _tp(dq), _tp(dk), _tp(dv), _tp(dm_unit),
                             _tp(dm_total), _stream(stream)))

@@ -73,3 +73,63 @@ def test_shard_partition(total, world):
         assert b == c and b >= a
     sizes = [b - a for a, b in spans]
     assert max(sizes) - min(sizes) <= 1
+
+
+def _bench_line(*argv):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *argv], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]  # exactly one JSON line (rank 0)
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("workload,strong", [("ml20m", True), ("ml1m", False)])
+def test_bench_launcher_spawns_ranks(workload, strong):
+    """`bench.py --gpus 2` outside torchrun re-executes itself under
+    torch.distributed.run with 2 ranks (gloo here): the line reports n_gpus 2,
+    the right global batch and shards that tile the batch."""
+    res = _bench_line("--gpus", "2", "--plan", "--workload", workload)
+    total_b = bench.WORKLOADS[workload][0]
+    assert res["n_gpus"] == 2
+    assert res["config"]["global_batch"] == (total_b if strong else 2 * total_b)
+    assert res["config"]["parallelism"].startswith("dp2")
+    if strong:
+        assert res["shards"] == [[0, total_b // 2], [total_b // 2, total_b]]
+    else:
+        assert res["shards"] == [[0, total_b], [0, total_b]]
+
+
+@pytest.mark.skipif(not oracle.ref_available(release=True), reason="oracle/_ref not built")
+def test_reference_arm_two_ranks_same_config():
+    """The reference arm under the launcher: rank 0 alone runs and prints, with
+    the config dict the GPU arm emits (workload_config)."""
+    res = _bench_line("--gpus", "2", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                      "--workload", "beauty")
+    assert res["impl"] == "reference" and res["n_gpus"] == 2
+    assert res["config"] == bench.workload_config("beauty", 2)
+    assert res["cpu_baseline"]["kind"] == "reference" and res["value"] > 0
+
+
+@pytest.mark.skipif(not oracle.ref_available(release=True), reason="oracle/_ref not built")
+def test_reference_arm_never_maps_the_product_library():
+    """--impl reference must not import the product package: after a full
+    reference-arm run, libcotten.so is absent from the process's mappings."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, argparse; sys.argv=['bench.py']; import bench; "
+            "a=argparse.Namespace(workload='beauty', steps=1, warmup=0); "
+            "r=bench.run_reference(a, 1, 0); assert r['value'] > 0; "
+            "maps=open('/proc/self/maps').read(); "
+            "assert 'libcotten' not in maps, 'product library mapped'; "
+            "assert 'paper_2602_06935_b200' not in sys.modules; print('clean')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "clean" in r.stdout, r.stderr[-2000:]
