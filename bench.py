@@ -248,6 +248,7 @@ def barrier(world):
 
 def run_ours(args, world, rank, local, with_cpu=True):
     import torch
+    import ctypes
     from paper_2602_06935_b200 import _lib, ops
     inputs = _inputs()
 
@@ -287,20 +288,21 @@ def run_ours(args, world, rank, local, with_cpu=True):
                      t["dk"], t["dv"], t["dm_unit"], dm_tot[i:i + 1], stream=s, flags=flags)
         launches[0] += _lib.launches()
 
-    n_marks = 2 * layers + 1
+    n_ops = 2 * layers
+    lib = _lib.load()
+    # Per-op kernel durations come from the kernels' own %globaltimer stamps
+    # (cotten_profile_begin): device-side, taken in the timed steps themselves,
+    # without event nodes between the ops (those would break the programmatic
+    # edges between the kernels and slow the step down, measured 12 %).
+    stamps = torch.empty((max(args.steps, 1), n_ops, 2), dtype=torch.int64, device=dev)
+    stamp_init = torch.tensor([2**63 - 1, 0], dtype=torch.int64, device=dev)
 
-    def step(s, marks=None):
-        """fwd of every layer, then bwd in reverse; marks[i] recorded after op i."""
-        if marks is not None:
-            marks[0].record(s)
+    def step(s):
+        """fwd of every layer, then bwd in reverse."""
         for i in range(layers):
             fwd(L[i], s)
-            if marks is not None:
-                marks[1 + i].record(s)
-        for j, i in enumerate(reversed(range(layers))):
+        for i in reversed(range(layers)):
             bwd(L[i], i, s)
-            if marks is not None:
-                marks[1 + layers + j].record(s)
 
     def allreduce_dm():
         if world > 1:  # the op's parameter-gradient exchange (dm per layer)
@@ -322,22 +324,22 @@ def run_ours(args, world, rank, local, with_cpu=True):
     # long steps measured ~4 % faster issued eagerly (ML-20M), so they stay eager.
     use_graph = args.graph == "on" or (args.graph == "auto" and eager_step_ms < 2.0)
 
-    gstep, gmarks = None, None
+    gstep, gstamps, step_launches = None, None, 0
     if use_graph:
-        # The whole step as ONE CUDA graph (inside a graph each kernel's
-        # programmatic-dependent-launch attribute becomes a programmatic edge),
-        # with external event-record nodes between the ops: the per-op kernel
-        # times behind `roofline` come from the very replays that are timed.
+        # The whole step as ONE CUDA graph: inside a graph each kernel's
+        # programmatic-dependent-launch attribute becomes a programmatic edge.
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
         with torch.cuda.stream(cap):
             step(cap)  # first use of the capture stream: its per-stream workspace
         cap.synchronize()
-        gmarks = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(n_marks)]
+        gstamps = torch.empty((n_ops, 2), dtype=torch.int64, device=dev)
         gstep = torch.cuda.CUDAGraph()
         launches[0] = 0
+        _lib.check(lib.cotten_profile_begin(ctypes.c_void_p(gstamps.data_ptr()), n_ops))
         with torch.cuda.graph(gstep, stream=cap):
-            step(torch.cuda.current_stream(), gmarks if args.graph_events else None)
+            step(torch.cuda.current_stream())
+        assert lib.cotten_profile_end() == n_ops
         step_launches = launches[0]
         stream.wait_stream(cap)
         torch.cuda.synchronize()
@@ -351,40 +353,29 @@ def run_ours(args, world, rank, local, with_cpu=True):
     barrier(world)
     torch.cuda.synchronize()
     launches[0] = 0
-    step_ms, op_ms = [], []
-    eager_marks = [[ev() for _ in range(n_marks)] for _ in range(args.steps)]
+    marks = [(ev(), ev()) for _ in range(args.steps)]
     for s_ in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps, outside the events
+        # outside the events: stamp reset and the L2 flush (256 MiB write)
+        st_buf = gstamps if use_graph else stamps[s_]
+        st_buf.copy_(stamp_init.expand(n_ops, 2))
+        flush.zero_()
+        marks[s_][0].record(stream)
         if use_graph:
-            if args.graph_events:
-                gstep.replay()
-                allreduce_dm()
-                torch.cuda.synchronize()  # read this replay's event nodes (outside the span)
-                mk = gmarks
-            else:
-                mk = eager_marks[s_]
-                mk[0].record(stream)
-                gstep.replay()
-                mk[-1].record(stream)
-                allreduce_dm()
+            gstep.replay()
             launches[0] += step_launches
         else:
-            mk = eager_marks[s_]
-            step(stream, mk)
-            allreduce_dm()
-            if world == 1:
-                continue
-        if use_graph and not args.graph_events:
-            continue
-        step_ms.append(mk[0].elapsed_time(mk[-1]))
-        op_ms.append([mk[i].elapsed_time(mk[i + 1]) for i in range(n_marks - 1)])
+            _lib.check(lib.cotten_profile_begin(ctypes.c_void_p(st_buf.data_ptr()), n_ops))
+            step(stream)
+            lib.cotten_profile_end()
+        marks[s_][1].record(stream)
+        allreduce_dm()
+        if use_graph:
+            stamps[s_].copy_(gstamps)  # after the end event: outside the span
     torch.cuda.synchronize()
-    if not step_ms:  # eager (world 1) / graph without event nodes: read after the loop
-        for mk in eager_marks:
-            step_ms.append(mk[0].elapsed_time(mk[-1]))
-            if not use_graph:
-                op_ms.append([mk[i].elapsed_time(mk[i + 1]) for i in range(n_marks - 1)])
     barrier(world)
+    step_ms = [a.elapsed_time(b) for a, b in marks]
+    st = stamps.cpu().numpy().astype(np.float64)
+    op_ms = ((st[..., 1] - st[..., 0]) / 1e6).tolist()  # [step][op] kernel durations
     gpu_launches = launches[0]
     graph_check = None
     if use_graph:
@@ -421,8 +412,7 @@ def run_ours(args, world, rank, local, with_cpu=True):
                 "shard": [lo, hi],
                 "launch": ("eager" if not use_graph else
                            "one CUDA graph per step (programmatic-dependent-launch edges between "
-                           "the kernels" + (", external event-record nodes between the ops)"
-                                            if args.graph_events else ")")),
+                           "the kernels)"),
                 "l2": "flushed between timed steps (256 MiB write), outside the events"},
         "gpu_launches": gpu_launches,
         "graph_outputs_equal_eager": graph_check,
@@ -439,7 +429,9 @@ def run_ours(args, world, rank, local, with_cpu=True):
             "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak, "traffic": None,
             "peak_source": peak_src, "algorithmic_bytes_per_launch": bwd_bytes,
             "avg_launch_us": bwd_avg * 1e6,
-            "timing": "CUDA events between the ops of the timed steps themselves"}
+            "timing": "kernel %globaltimer stamps (first CTA start after its dependency, last "
+                      "warp exit) in the timed steps themselves; step time from CUDA events",
+            "ops_sum_over_step": sum(map(sum, op_ms)) / sum(step_ms)}
         res["kernels"] = {"fwd_us": fwd_avg * 1e6, "fwd_GBps": fwd_gbs, "fwd_frac": fwd_gbs / peak,
                           "bwd_us": bwd_avg * 1e6, "bwd_GBps": bwd_gbs, "bwd_frac": bwd_gbs / peak,
                           "step_GBps": step_gbs, "step_frac": step_gbs / peak}
@@ -668,8 +660,6 @@ def main():
                     help="d_h=32 kernels: tcgen05 3xTF32 (default) or the FP32-pipe variant")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as one CUDA graph (auto: when the eager step < 2 ms)")
-    ap.add_argument("--no-graph-events", dest="graph_events", action="store_false",
-                    help="graph mode: no event nodes between the ops (step time only, no roofline)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-steady", action="store_true",
                     help="skip the ML-20M steady-state block appended to the default (ml1m) line")

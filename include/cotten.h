@@ -34,6 +34,12 @@
  *   base[b*stride_b + h*stride_h + i*stride_n + j]        (j contiguous).
  * All-zero strides select the contiguous [B][H][N][D] layout.  The mask is
  * uint8 valid[b*mask_stride_b + i] (0 = padded row), shared by all heads.
+ * Workspaces: the device entry points keep small grow-only device scratch per
+ * (device, stream) — per-unit dm, a recomputed S, the in-kernel dm total's
+ * CTA-completion counter — so concurrent calls on different streams never
+ * share it; calls on one stream are ordered.  The first call on a stream (or
+ * one needing more scratch) allocates, which CUDA-graph capture forbids: run
+ * one eager call on the stream before capturing it.
  * Saved state (optional in the forward, required by the backward):
  *   saved_S     [B*H][D][D]  accumulation type (float for f32/bf16, double for f64)
  *   saved_norms [B*H][2][N]  accumulation type: sqrt(|Q_i|^2+eps), then
@@ -122,6 +128,18 @@ int cotten_fwd_bwd_host(const cotten_desc* desc, const void* q, const void* k, c
 
 /* Number of kernel launches the last device call on this thread issued. */
 int cotten_last_launch_count(void);
+
+/* Launch-duration profile (measurement plumbing, no reference counterpart).
+ * After cotten_profile_begin(stamps, slots), the i-th device call
+ * (cotten_fwd / cotten_bwd) of the calling thread makes each of its kernels
+ * record, with atomics on the device buffer stamps[2*i .. 2*i+1] (uint64,
+ * caller-initialised to {UINT64_MAX or INT64_MAX, 0}), the earliest CTA start
+ * (after its programmatic dependency resolved) and the latest warp exit in
+ * %globaltimer ns.  The slot pointers are launch parameters, so a CUDA graph
+ * captured while profiling records into the same slots on every replay.
+ * cotten_profile_end() stops assigning slots and returns how many were used. */
+int cotten_profile_begin(void* stamps, int slots);
+int cotten_profile_end(void);
 
 #ifdef __cplusplus
 }

@@ -80,6 +80,8 @@ SIGNATURES = {
                                        _vp, _vp]),
     "cotten_fwd_bwd_host": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _dbl, _vp, _vp, _vp, _vp,
                                            _vp, _vp]),
+    "cotten_profile_begin": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "cotten_profile_end": (ctypes.c_int, []),
 }
 
 _lib = None

@@ -26,9 +26,29 @@ struct OpParams {
   void* workspace;       // kernel-specific global scratch (generic bwd: G per unit)
   double* dm_total;      // tcgen05 bwd: fixed-order sum of dm_unit, written by the last CTA
   unsigned* grid_done;   // tcgen05 bwd: zeroed CTA-completion counter (dm_total)
+  unsigned long long* tstamp;  // profiling (cotten_profile_begin): [0] min start, [1] max end (ns)
   int64_t B, H, N, D;
   int64_t sb, sh, sn, msb;
   double m, eps;
+};
+
+// Kernel time stamps from %globaltimer (ns) for the launch-duration profile
+// (cotten_profile_begin): the first CTA start (after its programmatic
+// dependency resolved) and the last warp exit, by atomics on a caller buffer
+// that is baked into a CUDA graph like every other launch parameter.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct KernelStamp {
+  unsigned long long* ts;
+  __device__ explicit KernelStamp(const OpParams& p) : ts(p.tstamp) {
+    if (ts && threadIdx.x == 0) atomicMin(ts, global_ns());
+  }
+  __device__ ~KernelStamp() {
+    if (ts && (threadIdx.x & 31) == 0) atomicMax(ts + 1, global_ns());
+  }
 };
 
 template <typename T>

@@ -26,6 +26,14 @@ namespace {
 
 thread_local std::string g_last_error;
 thread_local int g_launches = 0;
+// Launch-duration profile (cotten_profile_begin/end): each device call of this
+// thread takes the next [start, end] slot of the caller's buffer.
+struct Profile {
+  unsigned long long* buf = nullptr;
+  int slots = 0, next = 0;
+  unsigned long long* take() { return (buf && next < slots) ? buf + 2 * next++ : nullptr; }
+};
+thread_local Profile g_prof;
 
 struct Error {
   int code;
@@ -300,6 +308,7 @@ void device_fwd(const Layout& L, const void* q, const void* k, const void* v,
   p.saved_S = saved_S;
   p.saved_norms = saved_norms;
   p.status = device_status_word();
+  p.tstamp = g_prof.take();
   launch_fwd(L, p, st);
 }
 
@@ -316,6 +325,7 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
   p.valid = valid;
   p.m = m;
   p.status = device_status_word();
+  p.tstamp = g_prof.take();  // every kernel of this call stamps the same slot
   if (saved_S == nullptr) {  // recompute the state with an S-only forward
     void* s = scratch_get(st, kScrS, L.units() * L.D * L.D * acc_size(L.dtype));
     OpParams f = p;
@@ -513,6 +523,21 @@ int cotten_bwd(const cotten_desc* desc, const void* q, const void* k, const void
     device_bwd(L, q, k, v, valid, m, d_out, saved_S, dq, dk, dv, dm_unit, dm_total,
                (cudaStream_t)stream);
   });
+}
+
+int cotten_profile_begin(void* stamps, int slots) {
+  return guarded([&] {
+    if (stamps == nullptr || slots < 1) usage("cotten_profile_begin: null buffer or no slots");
+    g_prof.buf = static_cast<unsigned long long*>(stamps);
+    g_prof.slots = slots;
+    g_prof.next = 0;
+  });
+}
+
+int cotten_profile_end(void) {
+  const int used = g_prof.next;
+  g_prof = Profile{};
+  return used;
 }
 
 int cotten_device_status(int device, int32_t* bits, int reset) {

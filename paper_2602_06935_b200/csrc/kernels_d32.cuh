@@ -379,6 +379,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_fwd_d32_kernel(
     const __grid_constant__ CUtensorMap tv, const OpParams p,
     const __grid_constant__ ScaleTable tab) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  const KernelStamp stamp_(p);
   const int N = (int)p.N, H = (int)p.H;
   const int units = (int)(p.B * p.H);
   const Plan pl(N, NS, false);
@@ -555,6 +556,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
     const OpParams p, const __grid_constant__ ScaleTable tab) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  const KernelStamp stamp_(p);
   const int N = (int)p.N, H = (int)p.H;
   const int units = (int)(p.B * p.H);
   const Plan pl(N, NS, true);

@@ -75,6 +75,7 @@ __device__ void gen_fill_nan(const OpParams& p, T* dst, int64_t base) {
 // Forward (attention.cpp:297-395).  out == nullptr: only the saved state.
 template <typename T, typename A>
 __global__ void __launch_bounds__(kGenThreads) cos_fwd_generic(const OpParams p) {
+  const KernelStamp stamp_(p);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_cnt;
   const int D = (int)p.D;
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(kGenThreads) cos_fwd_generic(const OpParams p)
 // Backward (attention.cpp:397-441) given the saved S.
 template <typename T, typename A, bool GG>
 __global__ void __launch_bounds__(kGenThreads) cos_bwd_generic(const OpParams p) {
+  const KernelStamp stamp_(p);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_cnt;
   const int D = (int)p.D;

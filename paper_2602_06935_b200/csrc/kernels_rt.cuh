@@ -251,6 +251,7 @@ __device__ __forceinline__ void store_row(T* dst, const float (&o)[Cfg<D>::RC], 
 
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
+  const KernelStamp stamp_(p);
   using C = Cfg<D>;
   extern __shared__ __align__(16) float sm[];
   constexpr int TD = C::TR * C::LDT;
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
 
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
+  const KernelStamp stamp_(p);
   using C = Cfg<D>;
   extern __shared__ __align__(16) float sm[];
   constexpr int TD = C::TR * C::LDT;

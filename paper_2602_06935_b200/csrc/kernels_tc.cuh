@@ -840,6 +840,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
   if (threadIdx.x == 0) TC_TRACE_CTA(4);
   const uint32_t tmem = tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
   pdl_wait();
+  const KernelStamp stamp_(p);
   pdl_launch_dependents();
   if (threadIdx.x == 0) TC_TRACE_CTA(5);
 
@@ -1047,6 +1048,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
   if (threadIdx.x == 0) TC_TRACE_CTA(4);
   const uint32_t tmem = tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
   pdl_wait();
+  const KernelStamp stamp_(p);
   pdl_launch_dependents();
   if (threadIdx.x == 0) TC_TRACE_CTA(5);
 

@@ -6,7 +6,7 @@ The tcgen05 and FP32-pipe kernels run min(units, 148) persistent CTAs that
 loop over units (kernels_tc.cuh mask_loop / worker loops): with B*H >= 450
 every CTA runs >= 3 units, so the ring phase carried across units, the mask
 warp running ahead and the C == 1 operand reuse are all exercised.  Inputs are
-generated on the device; a sample of >= 64 units (every unit of four whole
+generated on the device; a sample of >= 64 units (every unit of eight whole
 CTAs, plus random ones) is compared with the oracle on the same fp32 (or
 bf16-rounded) values.  Tolerance: normwise <= 1e-5 (f32) / 1e-2 (bf16) per
 (sequence, head) tensor; padded dK / dV rows exactly 0.
@@ -34,11 +34,11 @@ def _torch():
     return torch
 
 
-def sample_units(units, grid, rng, n_random=32):
-    """Every unit of CTAs {0, 1, grid//2, grid-1} (strided by the grid), plus
+def sample_units(units, grid, rng, n_random=40):
+    """Every unit of 8 CTAs (first, last, spread; strided by the grid), plus
     random units: >= 64 units when units >= 3 * grid."""
     sel = set()
-    for c in {0, 1, grid // 2, grid - 1}:
+    for c in {0, 1, 2, grid // 4, grid // 2, 3 * grid // 4, grid - 2, grid - 1}:
         sel.update(range(c, units, grid))
     sel.update(int(u) for u in rng.choice(units, min(units, n_random), replace=False))
     return sorted(sel)
@@ -99,7 +99,7 @@ def test_tcgen05_multi_unit_schedule(N, B, H, m, mask_kind):
     t, res, dm_unit, dm_total = run_device(B, H, N, 32, valid, m, seed=N)
     rng = np.random.default_rng(N)
     units = sample_units(B * H, min(B * H, SMS), rng,
-                         n_random=16 if N >= 4096 else 32)
+                         n_random=16 if N >= 4096 else 48)
     if N >= 4096:  # fewer whole CTAs at long N (the oracle's N*d^2 loops)
         units = sorted(set(range(0, B * H, SMS)) | set(range(SMS - 1, B * H, SMS)) | set(units[:8])
                        | set(int(u) for u in rng.choice(B * H, 8, replace=False)))
