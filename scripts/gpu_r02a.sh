@@ -6,7 +6,7 @@ timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider -x --durations
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 400 python bench.py --impl reference > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
-timeout 400 python bench.py --no-graph-events --no-steady --no-cpu --no-e2e > gpurun_out/bench_noev.json 2>> gpurun_out/bench.err
+timeout 400 python bench.py --no-steady --no-cpu --no-e2e > gpurun_out/bench_noev.json 2>> gpurun_out/bench.err
 for p in tc tclong d32 rt64 rt128 rtbf16 generic; do
   for tool in memcheck racecheck synccheck; do
     timeout 600 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_case.py $p > gpurun_out/san/${tool}_$p.log 2>&1; echo "rc=$?" >> gpurun_out/san/${tool}_$p.log
