@@ -104,6 +104,18 @@ int cotten_bwd(const cotten_desc* desc, const void* q, const void* k, const void
                const uint8_t* valid, double m, const void* d_out, const void* saved_S,
                void* dq, void* dk, void* dv, double* dm_unit, double* dm_total, void* stream);
 
+/* The same two calls with the exponent m read from device memory (one double,
+ * e.g. a learnable per-layer parameter that an on-device optimizer updates:
+ * the encoder step in cotten_encoder.h never copies it to the host).  The
+ * SURVEY §8(b) proposal's `const float* m` argument. */
+int cotten_fwd_mdev(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                    const uint8_t* valid, const double* m_dev, void* out, void* saved_S,
+                    void* saved_norms, void* stream);
+int cotten_bwd_mdev(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                    const uint8_t* valid, const double* m_dev, const void* d_out,
+                    const void* saved_S, void* dq, void* dk, void* dv, double* dm_unit,
+                    double* dm_total, void* stream);
+
 /* Per-device sticky status word (COTTEN_STATUS_* bits); synchronises the
  * device.  reset != 0 clears it after reading. */
 int cotten_device_status(int device, int32_t* bits, int reset);

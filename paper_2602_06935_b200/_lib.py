@@ -74,6 +74,9 @@ SIGNATURES = {
     "cotten_fwd": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _dbl, _vp, _vp, _vp, _vp]),
     "cotten_bwd": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _dbl, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp]),
+    "cotten_fwd_mdev": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "cotten_bwd_mdev": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                       _vp, _vp, _vp]),
     "cotten_device_status": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_i32), ctypes.c_int]),
     "cotten_fwd_host": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _dbl, _vp, _vp, _vp]),
     "cotten_bwd_host": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _dbl, _vp, _vp, _vp, _vp, _vp,

@@ -31,14 +31,24 @@ def build_cuda(force=False, verbose_ptxas=False):
     """libcotten.so: every kernel + the C-ABI (include/cotten.h)."""
     out = os.path.join(PKG, "libcotten.so")
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    deps.append(os.path.join(ROOT, "include", "cotten.h"))
+    deps += [os.path.join(ROOT, "include", h) for h in ("cotten.h", "cotten_encoder.h")]
     if not force and not _stale(out, deps):
         return out
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-o", out, os.path.join(CSRC, "cotten_capi.cu")]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
     if verbose_ptxas:
-        cmd += ["-Xptxas", "-v"]
-    _run(cmd)
+        flags += ["-Xptxas", "-v"]
+    # one object per translation unit (rebuilt when its sources changed)
+    objs = []
+    for tu, tu_deps in (("cotten_capi.cu", [d for d in deps if not d.endswith("encoder.cu")
+                                            and not d.endswith("cotten_encoder.h")]),
+                        ("encoder.cu", [os.path.join(CSRC, "encoder.cu")] +
+                         [os.path.join(ROOT, "include", h) for h in ("cotten.h", "cotten_encoder.h")])):
+        obj = os.path.join(PKG, "build", tu.replace(".cu", ".o"))
+        os.makedirs(os.path.dirname(obj), exist_ok=True)
+        if force or _stale(obj, tu_deps):
+            _run([NVCC, *flags, "-c", "-o", obj, os.path.join(CSRC, tu)])
+        objs.append(obj)
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcublas"])
     return out
 
 

@@ -30,7 +30,12 @@ struct OpParams {
   int64_t B, H, N, D;
   int64_t sb, sh, sn, msb;
   double m, eps;
+  const double* m_dev;    // device-resident m (cotten_*_mdev): read by the kernels instead of m
 };
+
+// The exponent m of s = exp(-m ln true_n): the host value, or the device-resident
+// one (a learnable parameter updated on the device, encoder.cu) when given.
+__device__ __forceinline__ double op_m(const OpParams& p) { return p.m_dev ? *p.m_dev : p.m; }
 
 // Kernel time stamps from %globaltimer (ns) for the launch-duration profile
 // (cotten_profile_begin): the first CTA start (after its programmatic

@@ -294,16 +294,17 @@ void launch_bwd(const Layout& L, const OpParams& p, cudaStream_t st) {
 
 void device_fwd(const Layout& L, const void* q, const void* k, const void* v,
                 const uint8_t* valid, double m, void* out, void* saved_S, void* saved_norms,
-                cudaStream_t st) {
+                cudaStream_t st, const double* m_dev = nullptr) {
   if (!q || !k || !v) usage("cosine_attention_fused: null input");
   if (!out && !saved_S && !saved_norms) usage("cosine_attention_fused: no output requested");
-  if (!std::isfinite(m)) usage("cosine_attention_fused: m must be finite");
+  if (!m_dev && !std::isfinite(m)) usage("cosine_attention_fused: m must be finite");
   OpParams p = make_params(L);
   p.q = q;
   p.k = k;
   p.v = v;
   p.valid = valid;
   p.m = m;
+  p.m_dev = m_dev;
   p.out = out;
   p.saved_S = saved_S;
   p.saved_norms = saved_norms;
@@ -314,16 +315,18 @@ void device_fwd(const Layout& L, const void* q, const void* k, const void* v,
 
 void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
                 const uint8_t* valid, double m, const void* d_out, const void* saved_S, void* dq,
-                void* dk, void* dv, double* dm_unit, double* dm_total, cudaStream_t st) {
+                void* dk, void* dv, double* dm_unit, double* dm_total, cudaStream_t st,
+                const double* m_dev = nullptr) {
   if (!q || !k || !v || !d_out) usage("cosine_attention_backward: null input");
   if (!dq || !dk || !dv) usage("cosine_attention_backward: null gradient output");
-  if (!std::isfinite(m)) usage("cosine_attention_backward: m must be finite");
+  if (!m_dev && !std::isfinite(m)) usage("cosine_attention_backward: m must be finite");
   OpParams p = make_params(L);
   p.q = q;
   p.k = k;
   p.v = v;
   p.valid = valid;
   p.m = m;
+  p.m_dev = m_dev;
   p.status = device_status_word();
   p.tstamp = g_prof.take();  // every kernel of this call stamps the same slot
   if (saved_S == nullptr) {  // recompute the state with an S-only forward
@@ -355,6 +358,15 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
     COTTEN_CUDA(cudaGetLastError());
   }
 }
+
+}  // namespace
+
+// Shared with the encoder translation unit (encoder.cu): one thread-local
+// last-error string and one status word per device for the whole library.
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+int* status_word_for_current_device() { return device_status_word(); }
+
+namespace {
 
 // ---- host entry points ----------------------------------------------------
 
@@ -522,6 +534,30 @@ int cotten_bwd(const cotten_desc* desc, const void* q, const void* k, const void
     Layout L = resolve(desc, "cosine_attention_backward");
     device_bwd(L, q, k, v, valid, m, d_out, saved_S, dq, dk, dv, dm_unit, dm_total,
                (cudaStream_t)stream);
+  });
+}
+
+int cotten_fwd_mdev(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                    const uint8_t* valid, const double* m_dev, void* out, void* saved_S,
+                    void* saved_norms, void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    Layout L = resolve(desc, "cosine_attention_fused");
+    if (m_dev == nullptr) usage("cosine_attention_fused: null m_dev");
+    device_fwd(L, q, k, v, valid, 0.0, out, saved_S, saved_norms, (cudaStream_t)stream, m_dev);
+  });
+}
+
+int cotten_bwd_mdev(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                    const uint8_t* valid, const double* m_dev, const void* d_out,
+                    const void* saved_S, void* dq, void* dk, void* dv, double* dm_unit,
+                    double* dm_total, void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    Layout L = resolve(desc, "cosine_attention_backward");
+    if (m_dev == nullptr) usage("cosine_attention_backward: null m_dev");
+    device_bwd(L, q, k, v, valid, 0.0, d_out, saved_S, dq, dk, dv, dm_unit, dm_total,
+               (cudaStream_t)stream, m_dev);
   });
 }
 

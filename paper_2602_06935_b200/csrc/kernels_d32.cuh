@@ -517,7 +517,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_fwd_d32_kernel(
 
     // Pass 2 (:363-388): O = s * Q~ S for every row (padded rows included).
     uint8_t* Qt = ring + sq * pl.tb;
-    const float scale = tab.s[true_n];
+    const float scale = p.m_dev ? (float)exp(-*p.m_dev * log((double)true_n)) : tab.s[true_n];
     mbar_wait(&full[sq], phq);
     float2 o[4][4];
     row_output(Qt, Ss, r0, o, lane);
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
         for (int t = 0; t < 4; ++t) mbar_arrive(&empty[sl[t]]);
       continue;
     }
-    const float scale = tab.s[true_n];
+    const float scale = p.m_dev ? (float)exp(-*p.m_dev * log((double)true_n)) : tab.s[true_n];
 
     // Phase A: dQ (:410-411, :421-428) then G = Q~^T dO (:405), every row.
     mbar_wait(&full[sl[0]], ph[0]);
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) cos_bwd_d32_kernel(
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < NW; ++w) t += red[w];
-      if (p.dm_unit) p.dm_unit[u] = tab.coef[true_n] * t;  // -ln(n) s <G,S> (:408)
+      if (p.dm_unit) p.dm_unit[u] = (p.m_dev ? -log((double)true_n) * (double)(float)exp(-*p.m_dev * log((double)true_n)) : tab.coef[true_n]) * t;  // -ln(n) s <G,S> (:408)
       mbar_arrive(&empty[sl[2]]);
       mbar_arrive(&empty[sl[3]]);
     }

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kGenThreads) cos_fwd_generic(const OpParams p)
     if (p.out) gen_fill_nan<T, A>(p, static_cast<T*>(p.out), base);
     return;
   }
-  const A scale = (A)exp(-p.m * log((double)true_n));  // :303-304, in fp64
+  const A scale = (A)exp(-op_m(p) * log((double)true_n));  // :303-304, in fp64
   const A eps = (A)p.eps;
   const int nthr = blockDim.x;
   for (int e = threadIdx.x; e < D * D; e += nthr) S[e] = 0;
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kGenThreads) cos_bwd_generic(const OpParams p)
     return;
   }
   const double log_n = log((double)true_n);  // :402-403
-  const A scale = (A)exp(-p.m * log_n);
+  const A scale = (A)exp(-op_m(p) * log_n);
   const A eps = (A)p.eps;
 
   const A* srcS = static_cast<const A*>(p.saved_S) + unit * (int64_t)D * D;

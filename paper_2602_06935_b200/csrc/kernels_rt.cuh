@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
     if (p.out) gen_fill_nan<T, float>(p, static_cast<T*>(p.out), base);
     return;
   }
-  const float scale = (float)exp(-p.m * log((double)true_n));  // :303-304, in fp64
+  const float scale = (float)exp(-op_m(p) * log((double)true_n));  // :303-304, in fp64
   const float eps = (float)p.eps;
   const int tid = threadIdx.x, ab = tid / C::CB, cb = tid % C::CB;
   for (int e = tid; e < D * D; e += kThreads) Ssm[e] = 0.f;
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
     return;
   }
   const double log_n = log((double)true_n);  // :402-403
-  const float scale = (float)exp(-p.m * log_n);
+  const float scale = (float)exp(-op_m(p) * log_n);
   const float eps = (float)p.eps;
   const int tid = threadIdx.x, ab = tid / C::CB, cb = tid % C::CB, rb = ab;
 

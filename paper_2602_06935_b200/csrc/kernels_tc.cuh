@@ -482,7 +482,7 @@ __device__ __forceinline__ void mask_unit(const OpParams& p, int64_t b, uint32_t
     UnitConst c;
     c.tn = cnt;
     if (cnt > 0) {
-      unit_scale(p.m, cnt, &c.s, &c.coef);
+      unit_scale(op_m(p), cnt, &c.s, &c.coef);
     } else {  // UsageError in the reference (attention.cpp:44): NaN outputs + status bit
       c.s = __int_as_float(0x7fc00000);
       c.coef = __longlong_as_double(0x7ff8000000000000ll);
