@@ -465,6 +465,194 @@ def run_ours(args, world, rank, local, with_cpu=True):
     return res
 
 
+ENC_CFG = dict(vocab=3706, dim=64, layers=2, heads=2, max_seq=200, dropout=0.1)
+ENC_WORKLOAD = ("BASELINE config #2 in full: Cotten4Rec encoder training step on device - batch "
+                "assembly (fit_sequence + mask_sequence p=0.15), embedding, 2 post-norm blocks "
+                "(QKV projection -> cosine attention in place -> W_o, dropout 0.1, LN, FFN-GELU), "
+                "head over |V|+2=3708 ids, masked NLL, backward, clip + Adam; ML-1M shape "
+                "(B=256, N=200, d=64, H=2), fp32")
+
+
+def run_encoder(args, world, rank, local, with_cpu=True, B=256):
+    """The encoder training step of include/cotten_encoder.h (SURVEY §8(f)
+    rows 1-4) at the ML-1M shape: one step = assemble + forward + loss +
+    backward (+ NCCL all-reduce of the flat gradient buffer at N > 1) +
+    clip + Adam.  Inputs (ragged item histories, CSR) resident in HBM."""
+    import ctypes
+    import torch
+    from paper_2602_06935_b200 import _lib, encoder
+    cfg = encoder.ModelConfig(**ENC_CFG)
+    N = cfg.max_seq
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    rng = np.random.default_rng(1234 + rank)
+    # ML-1M-like histories: >= 20 ratings per user (ML-1M's filter), mean ~165,
+    # many longer than N (fit_sequence keeps the last N)
+    lens = np.clip(rng.geometric(1 / 150.0, size=B) + 19, 20, 2000)
+    offs = np.zeros(B + 1, np.int64)
+    offs[1:] = np.cumsum(lens)
+    items = rng.integers(1, cfg.vocab + 1, size=int(offs[-1])).astype(np.int32)
+    expect_k = 0.15 * np.minimum(lens, N).sum()
+    max_q = int(1.3 * expect_k) + 4 * B
+    enc = encoder.Encoder(cfg, max_batch=B, max_queries=max_q)
+    with torch.no_grad():  # init_encoder's recipe (encoder.cpp:26-60): N(0, .02) truncated at 2 sd
+        for i, (off, r, c) in enumerate(enc.layout):
+            t = enc.params[off:off + r * c]
+            if r == 1:
+                t.fill_(1.0 if (i - 2) % (3 * cfg.heads + 9) in (3 * cfg.heads + 5, 3 * cfg.heads + 7)
+                        and i < len(enc.layout) - 2 else 0.0)
+            else:
+                t.normal_(0.0, 0.02).clamp_(-0.04, 0.04)
+        enc.m.fill_(1.0)
+    d_items = torch.from_numpy(items).to(dev)
+    d_offs = torch.from_numpy(offs).to(dev)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    stamps = torch.empty((max(args.steps, 1), 2 * cfg.layers, 2), dtype=torch.int64, device=dev)
+    stamp_init = torch.tensor([2**63 - 1, 0], dtype=torch.int64, device=dev)
+    step_no = [0]
+
+    def step(items_t, offs_t, profile=None):
+        s = step_no[0]
+        step_no[0] += 1
+        ids, valid, rows, tg, k = enc.assemble(items_t, offs_t, N, train=True, p_mask=0.15, seed=s)
+        if profile is not None:
+            _lib.check(lib.cotten_profile_begin(ctypes.c_void_p(profile.data_ptr()),
+                                                2 * cfg.layers))
+        enc.model_forward(ids, rows, train=True, dropout_seed=s)
+        enc.nll_loss(tg, loss)
+        enc.model_backward()
+        if profile is not None:
+            lib.cotten_profile_end()
+        if world > 1:  # data-parallel step: one NCCL all-reduce of the flat gradients
+            import torch.distributed as dist
+            dist.all_reduce(enc.grads)
+            dist.all_reduce(enc.m_grads)
+            enc.grads.div_(world)
+            enc.m_grads.div_(world)
+        enc.clip_adam(max_norm=1.0, lr=1e-3, weight_decay=1e-3)
+
+    for _ in range(max(args.warmup, 3)):
+        step(d_items, d_offs)
+    torch.cuda.synchronize()
+    k_host = int((enc.assemble(d_items, d_offs, N, True, 0.15, seed=0)[4]).item())
+    # phase split of one instrumented (untimed) step
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ph = [ev() for _ in range(6)]
+    ph[0].record(stream)
+    ids, valid, rows, tg, k = enc.assemble(d_items, d_offs, N, True, 0.15, seed=1)
+    ph[1].record(stream)
+    enc.model_forward(ids, rows, train=True, dropout_seed=1)
+    ph[2].record(stream)
+    enc.nll_loss(tg, loss)
+    ph[3].record(stream)
+    enc.model_backward()
+    ph[4].record(stream)
+    enc.clip_adam(1.0, 1e-3, 1e-3)
+    ph[5].record(stream)
+    torch.cuda.synchronize()
+    names = ("assemble", "forward", "nll_loss", "backward", "clip_adam")
+    phases = {n: ph[i].elapsed_time(ph[i + 1]) for i, n in enumerate(names)}
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.25)
+    barrier(world)
+    torch.cuda.synchronize()
+    marks = [(ev(), ev()) for _ in range(args.steps)]
+    for s_ in range(args.steps):
+        stamps[s_].copy_(stamp_init.expand(2 * cfg.layers, 2))
+        flush.zero_()
+        marks[s_][0].record(stream)
+        step(d_items, d_offs, profile=stamps[s_])
+        marks[s_][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    step_ms = [a.elapsed_time(b) for a, b in marks]
+    clocks = sampler.stop()
+    total_ms = max_over_ranks(sum(step_ms), world)
+    ms = total_ms / args.steps
+    st = stamps.cpu().numpy().astype(np.float64)
+    op_us = (st[..., 1] - st[..., 0]) / 1e3  # [step][fwd l0, fwd l1, bwd l1, bwd l0]
+    L_ = cfg.layers
+    fwd_us = float(op_us[:, :L_].mean())
+    bwd_us = float(op_us[:, L_:].mean())
+    fb, bb = algorithmic_bytes(B, cfg.heads, N, cfg.dim // cfg.heads)
+    peak, peak_src = load_peaks()
+    res = {
+        "workload": ENC_WORKLOAD, "value": B * world * args.steps / (total_ms / 1e3),
+        "unit": "seq/s", "n_gpus": world, "ms_per_step": ms, "steps": args.steps,
+        "queries_per_step": k_host, "dtype": "f32",
+        "parallelism": f"dp{world}" + (" (NCCL all-reduce of the flat gradient buffer)"
+                                       if world > 1 else ""),
+        "phases_ms": phases, "clocks": clocks,
+        "op_kernels": {
+            "fwd_us": fwd_us, "bwd_us": bwd_us, "fwd_frac": fb / (fwd_us * 1e-6) / 1e9 / peak,
+            "bwd_frac": bb / (bwd_us * 1e-6) / 1e9 / peak,
+            "share_of_step": float(op_us.sum(axis=1).mean() / 1e3 / ms),
+            "note": "cosine-attention kernels inside the step (%globaltimer stamps); the "
+                    "projections' cuBLAS GEMMs and the other kernels are the rest"},
+        "roofline": {"bound": "hbm", "kernel": "cos_bwd inside the encoder step",
+                     "achieved": bb / (bwd_us * 1e-6) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": bb / (bwd_us * 1e-6) / 1e9 / peak, "traffic": None,
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": bb},
+    }
+    # end to end: ragged histories uploaded from pinned host memory every step,
+    # the loss read back (both inside the timed region)
+    h_items = torch.from_numpy(items).pin_memory()
+    h_offs = torch.from_numpy(offs).pin_memory()
+    h_loss = torch.empty(1, dtype=torch.float64).pin_memory()
+    e_items = torch.empty_like(d_items)
+    e_offs = torch.empty_like(d_offs)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e_items.copy_(h_items, non_blocking=True)
+        e_offs.copy_(h_offs, non_blocking=True)
+        step(e_items, e_offs)
+        h_loss.copy_(loss, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    res["e2e"] = {"value": B * world * args.steps / e2e_s, "unit": "seq/s",
+                  "h2d_bytes_per_step": int(items.nbytes + offs.nbytes), "d2h_bytes_per_step": 8,
+                  "path": "Encoder.assemble/model_forward/nll_loss/model_backward/clip_adam "
+                          "(include/cotten_encoder.h), host wall clock, loss read back per step"}
+    if with_cpu and rank == 0 and world == 1:
+        res["cpu_baseline"] = run_encoder_cpu(cfg, items, offs, N)
+    return res
+
+
+def run_encoder_cpu(cfg, items, offs, N, sample=32, reps=3):
+    """The reference's own training step (model_forward + nll_loss +
+    model_backward + clip_gradients + adam_step, cfg.threads = all host
+    threads) on a bounded subsample of the same batch."""
+    import oracle.encoder_ref as eref
+    if not eref.available():
+        return {"value": None, "unavailable": "oracle/_ref/libcosrec_encoder.so not built"}
+    rng = np.random.default_rng(7)
+    ids = np.zeros((sample, N), np.int32)
+    positions, targets = [], []
+    for b in range(sample):
+        s = items[offs[b]:offs[b + 1]][-N:]
+        ids[b, N - len(s):] = s
+        real = np.arange(N - len(s), N)
+        k = max(1, int(round(0.15 * len(s))))
+        pos = np.sort(rng.choice(real, size=k, replace=False))
+        positions.append(pos.tolist())
+        targets += ids[b, pos].tolist()
+        ids[b, pos] = cfg.vocab + 1
+    threads = os.cpu_count() or 1
+    secs = eref.bench(cfg, threads, ids, positions, np.array(targets, np.int32), reps)
+    return {"value": sample / float(np.median(secs)), "unit": "seq/s", "cores": threads,
+            "kind": "reference",
+            "sample": f"{sample} of the batch's sequences (same histories, p_mask 0.15), "
+                      f"median of {reps} reference training steps (model_forward + nll_loss + "
+                      f"model_backward + clip + Adam, oracle/_ref/libcosrec_encoder.so -O2), "
+                      f"cfg.threads={threads}"}
+
+
 def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
     """Same metric through the reference-facing host entry points
     (cotten_fwd_host / cotten_bwd_host: the calls under cosine_attention_fused /
@@ -664,6 +852,10 @@ def main():
     ap.add_argument("--no-steady", action="store_true",
                     help="skip the ML-20M steady-state block appended to the default (ml1m) line")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-encoder", action="store_true",
+                    help="skip the encoder training-step block (config #2 in full)")
+    ap.add_argument("--encoder-only", action="store_true",
+                    help="run only the encoder training step (its own line)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--plan", action="store_true", help="print the shard plan only (no GPU)")
     args = ap.parse_args()
@@ -675,6 +867,10 @@ def main():
         res = run_plan(args, world, rank)
     elif args.impl == "reference":
         res = run_reference(args, world, rank)
+    elif args.encoder_only:
+        res = run_encoder(args, world, rank, local, with_cpu=not args.no_cpu)
+        if rank != 0:
+            res = None
     else:
         res = run_ours(args, world, rank, local)
         if (world == 1 and args.workload == "ml1m" and not args.no_steady and res is not None):
@@ -695,6 +891,14 @@ def main():
                 "roofline": r2["roofline"], "clocks": r2["clocks"]}
             if not args.no_cpu:
                 res["steady_state"]["cpu_baseline"] = run_cpu_baseline("ml20m", args.cpu_seconds / 2)
+            torch.cuda.empty_cache()
+        if res is not None and args.workload == "ml1m" and not args.no_encoder:
+            # BASELINE config #2 in full: the encoder step around the op (§8(f))
+            import torch
+            a3 = argparse.Namespace(**vars(args))
+            a3.steps, a3.warmup = min(args.steps, 10), 3
+            res["encoder_step"] = run_encoder(a3, world, rank, local,
+                                              with_cpu=not args.no_cpu and world == 1)
             torch.cuda.empty_cache()
     if rank == 0 and res is not None:
         print(json.dumps(res), flush=True)

@@ -8,7 +8,7 @@
  *   cotten_enc_assemble      make_batches/fit_sequence (data.cpp:193-222),
  *                            mask_sequence (training.cpp:15-56) and
  *                            mask_for_ids (encoder.cpp:268-272)
- *   cotten_enc_forward       model_forward (encoder.cpp:276-325): embed (:78-94),
+ *   cotten_enc_forward       model_forward (encoder.cpp:276-325): embed (:80-95),
  *                            block_forward (:183-219) x layers — multi-head
  *                            attention (attention.cpp:487-526: fused QKV
  *                            projection -> cotten_fwd on the projection output
@@ -55,7 +55,7 @@ typedef struct cotten_enc_config {
   int64_t layers;   /* L */
   int64_t heads;    /* H (AttentionConfig::heads); d % H == 0 */
   int64_t max_seq;  /* position-embedding rows; every batch has N <= max_seq */
-  double dropout;   /* p (inverted dropout, encoder.cpp:157-165) */
+  double dropout;   /* p (inverted dropout, encoder.cpp:159-165) */
   double ln_eps;    /* layer-norm eps (encoder.hpp:25) */
   double attn_eps;  /* AttentionConfig::eps */
 } cotten_enc_config;
@@ -69,7 +69,7 @@ int cotten_enc_create(const cotten_enc_config* cfg, int64_t max_batch, int64_t m
                       cotten_encoder** out);
 int cotten_enc_destroy(cotten_encoder* enc);
 
-/* Flat layout: n_tensors = 4 + 12*L + 3*H*L... (see cotten_enc_layout);
+/* Flat layout: n_tensors = 4 + L*(3H + 9) (see cotten_enc_layout);
  * offsets[i] is the float offset of tensor i, offsets[n] = the float count;
  * the L doubles of m follow at cotten_enc_m_params / cotten_enc_m_grads. */
 int64_t cotten_enc_tensor_count(const cotten_encoder* enc);

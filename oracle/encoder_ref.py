@@ -43,6 +43,8 @@ def lib():
         L.ref_enc_clip_adam.argtypes = [_i64] * 5 + [_vp] * 8 + [_long, _dbl, _dbl, _dbl, _vp]
         L.ref_fit_mask_eval.restype = _int
         L.ref_fit_mask_eval.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]
+        L.ref_enc_bench.restype = _int
+        L.ref_enc_bench.argtypes = [_i64] * 5 + [_dbl, _i64, _i64, _i64] + [_vp] * 4 + [_int, _vp]
         _lib = L
     return _lib
 
@@ -111,3 +113,17 @@ def fit_mask_eval(items, offsets, n, vocab):
                                    _p(np.ascontiguousarray(offsets, np.int64)), B, n, vocab,
                                    _p(ids), _p(slot), _p(tg)))
     return ids, slot, tg
+
+
+def bench(cfg, threads, ids, positions, targets, reps):
+    """Per-rep seconds of the reference's training step on this batch
+    (model_forward + nll_loss + model_backward + clip + Adam, cfg.threads)."""
+    B, n = ids.shape
+    off = np.zeros(B + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in positions])
+    pos = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int64) for p in positions]))
+    secs = np.empty(reps, np.float64)
+    _check(lib().ref_enc_bench(*dims(cfg), cfg.dropout, threads, B, n,
+                               _p(np.ascontiguousarray(ids, np.int32)), _p(off), _p(pos),
+                               _p(np.ascontiguousarray(targets, np.int32)), reps, _p(secs)))
+    return secs

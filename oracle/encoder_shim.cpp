@@ -16,6 +16,7 @@
 //   ref_enc_clip_adam   clip_gradients + adam_step (training.cpp:89-143)
 //   ref_fit_mask_eval   fit_sequence (data.cpp:193-199) + mask_sequence eval
 //                       (training.cpp:15-56)
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -193,6 +194,44 @@ int ref_fit_mask_eval(const int32_t* items, const int64_t* offs, int64_t B, int6
       std::memcpy(ids_out + b * n, ms.seq.data(), n * sizeof(int32_t));
       slot_out[b] = (int64_t)ms.positions[0];
       target_out[b] = ms.targets[0];
+    }
+  });
+}
+
+// The timed CPU arm of bench.py's encoder line: `reps` training steps of the
+// reference on one batch — model_forward (cfg.threads workers, encoder.cpp:295)
+// + nll_loss + model_backward (:345) + clip_gradients + adam_step, exactly the
+// body of train()'s batch loop (training.cpp:176-189).  Per-rep wall seconds
+// into secs_out.
+int ref_enc_bench(int64_t vocab, int64_t dim, int64_t layers, int64_t heads, int64_t max_seq,
+                  double dropout, int64_t threads, int64_t B, int64_t n, const int32_t* ids,
+                  const int64_t* pos_off, const int64_t* positions, const int32_t* targets,
+                  int reps, double* secs_out) {
+  return guarded([&] {
+    ModelConfig c = make_cfg(vocab, dim, layers, heads, max_seq, dropout, 1e-5, 1e-6);
+    c.threads = (std::size_t)threads;
+    EncoderParams p = init_encoder(c, 0);
+    AdamState st = make_adam_state(p);
+    SequenceBatch sb;
+    std::vector<int32_t> tg;
+    for (int64_t b = 0; b < B; ++b) {
+      sb.ids.emplace_back(ids + b * n, ids + (b + 1) * n);
+      std::vector<std::size_t> pos;
+      for (int64_t k = pos_off[b]; k < pos_off[b + 1]; ++k) {
+        pos.push_back((std::size_t)positions[k]);
+        tg.push_back(targets[k]);
+      }
+      sb.positions.push_back(std::move(pos));
+    }
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      ForwardOut f = model_forward(sb, p, c, true, (uint64_t)r);
+      LossOut lo = nll_loss(f.logits, tg);
+      EncoderParams g = model_backward(f.cache, p, c, lo.d_logits);
+      clip_gradients(g, 1.0);
+      adam_step(p, g, st, 1e-3, 1e-3);
+      const auto t1 = std::chrono::steady_clock::now();
+      secs_out[r] = std::chrono::duration<double>(t1 - t0).count();
     }
   });
 }
