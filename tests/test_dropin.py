@@ -70,6 +70,30 @@ def test_reference_encoder_with_b200_operator_matches(tmp_path, dtype, tol):
     calls = int(re.search(r"adapter_calls=(\d+)", out).group(1))
     # 2 layers x 2 heads x 6 sequences, forward and backward
     assert calls >= 2 * 2 * 6 * 2
+    # AttentionByteProbe through the drop-in: the adapter's host staging is
+    # tracked, so the epoch probe reads > 0 (test_training.cpp:269-272)
+    assert int(re.search(r"probe_peak=(\d+)", out).group(1)) > 0
     assert ref.shape == gpu.shape and np.isfinite(gpu).all()
     err = np.abs(gpu - ref).max() / np.abs(ref).max()
     assert err <= tol, f"{dtype}: normwise {err:.3e}"
+
+
+@needs_build
+@pytest.mark.gpu
+def test_reference_encoder_at_ml1m_shape_reaches_tcgen05(tmp_path):
+    """The reference encoder at the ML-1M shape (N=200, d=64, H=2, |V|=3706,
+    dropout 0.1 from the reference's own RNG in both runs): through the
+    adapter every head call is a N=200, d_h=32 unit, i.e. the tcgen05
+    kernels; logits and every gradient match the pure reference."""
+    def run(exe, path, env=None):
+        r = subprocess.run([exe, str(path), "8", "bench", "8", "1"], capture_output=True,
+                           text=True, timeout=600, env=env)
+        assert r.returncode == 0, r.stdout + r.stderr
+        return np.fromfile(path, dtype=np.float64), r.stdout
+    ref, _ = run(os.path.join(BUILD, "dropin_ref"), tmp_path / "ref.bin")
+    gpu, out = run(os.path.join(BUILD, "dropin_gpu"), tmp_path / "gpu.bin",
+                   dict(os.environ, COTTEN_ADAPTER_DTYPE="f32"))
+    assert int(re.search(r"adapter_calls=(\d+)", out).group(1)) >= 2 * 2 * 8 * 2 * 2
+    assert ref.shape == gpu.shape and np.isfinite(gpu).all()
+    err = np.abs(gpu - ref).max() / np.abs(ref).max()
+    assert err <= 2e-4, f"normwise {err:.3e}"
