@@ -20,6 +20,7 @@
 #include "kernels_generic.cuh"
 #include "kernels_rt.cuh"
 #include "kernels_tc.cuh"
+#include "kernels_tcb.cuh"
 
 namespace cotten {
 namespace {
@@ -222,7 +223,12 @@ template <typename T>
 void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
-  if (tensor && tc_fwd_supported<T>(p)) {
+  if (tensor && tcb_fwd_supported<T>(p)) {
+    const int n = launch_tcb_fwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: bf16 tensor-core forward launch failed"};
+    g_launches += n;
+  } else if (tensor && tc_fwd_supported<T>(p)) {
     const int n = launch_tc_fwd(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: tensor-core forward launch failed"};
@@ -250,7 +256,12 @@ template <typename T>
 void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
-  if (tensor && tc_bwd_supported<T>(p)) {
+  if (tensor && tcb_bwd_supported<T>(p)) {
+    const int n = launch_tcb_bwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: bf16 tensor-core backward launch failed"};
+    g_launches += n;
+  } else if (tensor && tc_bwd_supported<T>(p)) {
     const int n = launch_tc_bwd(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: tensor-core backward launch failed"};
@@ -344,9 +355,9 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
   p.dm_unit = dm_unit;
   if (dm_total && !dm_unit)
     p.dm_unit = static_cast<double*>(scratch_get(st, kScrDm, L.units() * sizeof(double)));
-  const bool tc_path = L.dtype == COTTEN_F32 &&
-                       !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE)) &&
-                       tc_bwd_supported<float>(p);
+  const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
+  const bool tc_path = tensor && ((L.dtype == COTTEN_F32 && tc_bwd_supported<float>(p)) ||
+                                  (L.dtype == COTTEN_BF16 && tcb_bwd_supported<__nv_bfloat16>(p)));
   if (dm_total && tc_path) {  // the tcgen05 kernel's last CTA writes the total (no extra launch)
     p.dm_total = dm_total;
     p.grid_done = static_cast<unsigned*>(scratch_get(st, kScrCounter, sizeof(unsigned), true));

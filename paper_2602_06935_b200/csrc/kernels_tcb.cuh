@@ -1,0 +1,887 @@
+// Tensor-core (tcgen05 kind::f16) cosine-attention kernels for bf16 inputs,
+// head_dim 64, any seq_len up to 16384 — BASELINE config #5's bf16 points
+// (north star: "tcgen05/TMEM tiles for the two small contractions ... at
+// d_head >= 64"; the FP32-pipe kernels_rt.cuh is the A/B alternative).
+//
+// bf16 data in HBM, fp32 arithmetic everywhere; every value computed in
+// fp32 that enters an MMA — the normalised rows q~ / k~ and the d_h x d_h
+// state (S, dA = s G) — is a bf16 hi / lo pair (x = hi + lo to ~2^-17), and
+// the MMAs accumulate hi*hi + hi*lo + lo*hi in fp32 TMEM ("bf16x3"; V and dO
+// are bf16 already, so their products need hi only).  A single bf16 rounding
+// of q~ / k~ is not enough: at N = 1, O = (q~.k~) v cancels and the 2^-9
+// rounding grows to ~2e-2 (measured), over the 1e-2 bar.  The lo half of
+// q~ / k~ overwrites the raw row in the TMA stage (each splitter thread owns
+// its row), so no extra shared memory is needed; the epiloguer rebuilds
+// q~ / k~ = hi + lo in fp32 for the row Jacobians, with 1/norm handed over in
+// a TMEM column.
+//
+// Same persistent warp-role pipeline as the fp32 kernels (kernels_tc.cuh):
+// 128-row chunks, one TMA box (64 bf16 x 128 rows = 16 KB, SWIZZLE_128B) per
+// tensor per chunk, a 3-slot ring; per slot a raw stage (X, Y) and one
+// "normalised" tile Z (q~ or k~ in bf16) that later stages the chunk's
+// outputs for the TMA store.
+//   forward   pass 1 (K, V):  Z|X = k~ hi|lo (masked);  S += (Z + X)^T Y    (M = N = 64, K = 16 rows)
+//             pass 2 (Q):     Z|X = q~ hi|lo;           O = s (Z + X) S     (M = 128, N = 64, K = 64)
+//   backward  pass 1 (Q, dO): Z|X = q~ hi|lo (r < N);   G += (Z + X)^T Y,  dQ~ = s Y S^T
+//             pass 2 (K, V):  Z|X = k~ hi|lo (masked);  dV = (Z + X) dA,  dK~ = Y dA^T  (dA = s G)
+// (attention.cpp:297-395, :397-441).  Operand conventions (measured in
+// scripts/dev/mma_probe_bf16.cu): a 128-B-row SW128 tile is both the
+// MN-major operand of a reduction (rows = K) and the K-major operand of a
+// row output (rows = M); the 64 x 64 state tiles (S or dA rows, bf16) are the
+// MN-major B of O = Q~ S / dV = K~ dA and the K-major B of dQ~ = dO S^T /
+// dK~ = V dA^T alike.
+//
+// Warp roles (384 threads): 0-3 splitter (thread t = chunk row t), 4-7
+// epiloguer (thread t = TMEM lane t), 8 TMA producer, 9 MMA issuer, 10 mask
+// warp, 11 store warp (TMA stores, then frees the whole slot).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels_tc.cuh"
+
+namespace cotten {
+namespace tcb {
+
+using d32::mbar_arrive;
+using d32::mbar_expect_tx;
+using d32::mbar_init;
+using d32::mbar_wait;
+using d32::smem_u32;
+using d32::tma_load_4d;
+using tc::bulk_wait0;
+using tc::bulk_wait_read0;
+using tc::elect_one;
+using tc::fence_proxy_async;
+using tc::mma_commit;
+using tc::tc_fence_after;
+using tc::tc_fence_before;
+using tc::tma_store_4d;
+using tc::tmem_ld32;
+using tc::tmem_wait_ld;
+using tc::UnitConst;
+
+constexpr int kD = 64;
+constexpr int kRows = 128;
+constexpr uint32_t kTile = 16384;  // 128 rows x 128 B
+constexpr int kRing = 3;
+constexpr int kMaxN = 16384;
+constexpr int kFlush = 4;  // S / G accumulator flushed every 4 chunks (<= 32 MMAs per chain)
+constexpr int kWarpProducer = 8, kWarpMma = 9, kWarpMask = 10, kWarpStore = 11;
+constexpr int kThreads = 12 * 32;
+
+// shared memory: per slot X, Y (raw TMA tiles) and Z (normalised / staging)
+constexpr uint32_t kSlot = 3 * kTile;
+constexpr uint32_t kOffRing = 0;
+constexpr uint32_t kStateTile = 64 * 128;  // 64 x 64 bf16 rows
+constexpr uint32_t kOffOps = kOffRing + kRing * kSlot;   // S hi, S lo, dA hi, dA lo
+constexpr uint32_t kOffRun = kOffOps + 4 * kStateTile;   // fp32 running sum, 64 x 64
+constexpr uint32_t kOffFlags = kOffRun + 64 * 64 * 4;    // 2 x 2 KB bitmasks
+constexpr uint32_t kOffMisc = kOffFlags + 2 * (kMaxN / 8);
+constexpr uint32_t kOffBar = kOffMisc + 128;
+constexpr uint32_t kSmemBytes = kOffBar + 32 * 8;
+static_assert(kSmemBytes <= 227 * 1024, "shared-memory budget");
+
+// TMEM: [0, 64) the S / G accumulator (M = 64: row m at lane (m % 16) + 32 (m / 16));
+// slot b at 64 + 128 b: [+0, +64) O | dQ~ | dV, [+64, +128) dK~.
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kBuf0 = 64;
+constexpr uint32_t kBufCols = 128;
+constexpr uint32_t kInv = kBuf0 + kRing * kBufCols;  // + slot: the row's 1/norm (bwd)
+
+__device__ __forceinline__ int slot3(int it) { return it % kRing; }
+__device__ __forceinline__ uint32_t par3(int it) { return (uint32_t)(it / kRing) & 1u; }
+
+struct Bars {
+  uint64_t raw_full[kRing], slot_free[kRing], split_full[kRing], mma_done[kRing], staged[kRing];
+  uint64_t op_ready, acc_free, red_done;
+  uint64_t fl_full[2], fl_empty[2];
+};
+static_assert(sizeof(Bars) <= 256, "barrier area");
+
+// ---- bf16 rows of a 128-B SW128 tile (16-byte granule j of row r at j ^ (r & 7)) ----
+__device__ __forceinline__ uint32_t goff(int row, int j) {
+  return (uint32_t)row * 128u + ((uint32_t)(j ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ void load_row(const uint8_t* tile, int row, float (&x)[64]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 v = *reinterpret_cast<const uint4*>(tile + goff(row, j));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      x[8 * j + 2 * e] = f.x;
+      x[8 * j + 2 * e + 1] = f.y;
+    }
+  }
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void store_row(uint8_t* tile, int row, const float (&x)[64]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<uint4*>(tile + goff(row, j)) =
+        make_uint4(pack2(x[8 * j], x[8 * j + 1]), pack2(x[8 * j + 2], x[8 * j + 3]),
+                   pack2(x[8 * j + 4], x[8 * j + 5]), pack2(x[8 * j + 6], x[8 * j + 7]));
+}
+// x = hi + lo as two bf16 rows: hi into `hi_tile`, lo into `lo_tile`
+__device__ __forceinline__ void store_split_row(uint8_t* hi_tile, uint8_t* lo_tile, int row,
+                                                const float (&x)[64]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float h[8], l[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      h[e] = __bfloat162float(__float2bfloat16_rn(x[8 * j + e]));
+      l[e] = x[8 * j + e] - h[e];
+    }
+    *reinterpret_cast<uint4*>(hi_tile + goff(row, j)) =
+        make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7]));
+    *reinterpret_cast<uint4*>(lo_tile + goff(row, j)) =
+        make_uint4(pack2(l[0], l[1]), pack2(l[2], l[3]), pack2(l[4], l[5]), pack2(l[6], l[7]));
+  }
+}
+// hi + lo rows back to fp32
+__device__ __forceinline__ void load_split_row(const uint8_t* hi_tile, const uint8_t* lo_tile,
+                                               int row, float (&x)[64]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 vh = *reinterpret_cast<const uint4*>(hi_tile + goff(row, j));
+    const uint4 vl = *reinterpret_cast<const uint4*>(lo_tile + goff(row, j));
+    const uint32_t wh[4] = {vh.x, vh.y, vh.z, vh.w}, wl[4] = {vl.x, vl.y, vl.z, vl.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 fh = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wh[e]));
+      const float2 fl = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wl[e]));
+      x[8 * j + 2 * e] = fh.x + fl.x;
+      x[8 * j + 2 * e + 1] = fh.y + fl.y;
+    }
+  }
+}
+__device__ __forceinline__ float sumsq64(const float (&x)[64]) {
+  float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+#pragma unroll
+  for (int k = 0; k < 64; k += 4) {
+    a = fmaf(x[k], x[k], a);
+    b = fmaf(x[k + 1], x[k + 1], b);
+    c = fmaf(x[k + 2], x[k + 2], c);
+    d = fmaf(x[k + 3], x[k + 3], d);
+  }
+  return (a + b) + (c + d);
+}
+__device__ __forceinline__ float dot64(const float (&x)[64], const float (&y)[64]) {
+  float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+#pragma unroll
+  for (int k = 0; k < 64; k += 4) {
+    a = fmaf(x[k], y[k], a);
+    b = fmaf(x[k + 1], y[k + 1], b);
+    c = fmaf(x[k + 2], y[k + 2], c);
+    d = fmaf(x[k + 3], y[k + 3], d);
+  }
+  return (a + b) + (c + d);
+}
+// 64 accumulator columns of this thread's lane
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&r)[64]) {
+  float* a = r;
+  tmem_ld32(taddr, *reinterpret_cast<float(*)[32]>(a));
+  tmem_ld32(taddr + 32, *reinterpret_cast<float(*)[32]>(a + 32));
+  tmem_wait_ld();
+}
+// Row a of a 64 x 64 state matrix as bf16 hi / lo rows (x = hi + lo).
+__device__ __forceinline__ void store_state_row(uint8_t* hi, uint8_t* lo, int a,
+                                                const float (&x)[64]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float h[8], l[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      h[e] = __bfloat162float(__float2bfloat16_rn(x[8 * j + e]));
+      l[e] = x[8 * j + e] - h[e];
+    }
+    *reinterpret_cast<uint4*>(hi + goff(a, j)) =
+        make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7]));
+    *reinterpret_cast<uint4*>(lo + goff(a, j)) =
+        make_uint4(pack2(l[0], l[1]), pack2(l[2], l[3]), pack2(l[4], l[5]), pack2(l[6], l[7]));
+  }
+}
+// <x, hi + lo> for row a of a state tile pair, one granule at a time
+__device__ __forceinline__ float dot_state_row(const uint8_t* hi, const uint8_t* lo, int a,
+                                               const float (&x)[64]) {
+  float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 vh = *reinterpret_cast<const uint4*>(hi + goff(a, j));
+    const uint4 vl = *reinterpret_cast<const uint4*>(lo + goff(a, j));
+    const uint32_t wh[4] = {vh.x, vh.y, vh.z, vh.w}, wl[4] = {vl.x, vl.y, vl.z, vl.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 fh = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wh[e]));
+      const float2 fl = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wl[e]));
+      d0 = fmaf(x[8 * j + 2 * e], fh.x + fl.x, d0);
+      d1 = fmaf(x[8 * j + 2 * e + 1], fh.y + fl.y, d1);
+    }
+  }
+  return d0 + d1;
+}
+
+// ---- MMA issue ------------------------------------------------------------------
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);  // SWIZZLE_128B
+}
+__device__ __forceinline__ uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  // D fp32, A / B bf16
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// R (M = N = 64) += x^T y over `ksteps` 16-row groups of two MN-major tiles
+__device__ __forceinline__ void issue_reduction(uint32_t d, uint32_t x, uint32_t y, int ksteps,
+                                                bool first) {
+  const uint32_t id = idesc_bf16(64, 64, true, true);
+  for (int kk = 0; kk < ksteps; ++kk)
+    mma_bf16(d, sdesc(x + 2048u * kk, kTile, 1024u), sdesc(y + 2048u * kk, kTile, 1024u), id,
+             (first && kk == 0) ? 0u : 1u);
+}
+// D (128 x 64) = A (K-major chunk tile, K = 64 features) x B (state hi + lo):
+// B MN-major (rows = k) for O = Q~ S, dV = K~ dA; K-major (rows = n) for
+// dQ~ = dO S^T, dK~ = V dA^T.
+template <bool kBMN>
+__device__ __forceinline__ void issue_rowout(uint32_t d, uint32_t a, uint32_t bh, uint32_t bl) {
+  const uint32_t id = idesc_bf16(128, 64, false, kBMN);
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const uint64_t ad = sdesc(a + 32u * kk, 16u, 1024u);
+    const uint64_t dh = kBMN ? sdesc(bh + 2048u * kk, kTile, 1024u) : sdesc(bh + 32u * kk, 16u, 1024u);
+    const uint64_t dl = kBMN ? sdesc(bl + 2048u * kk, kTile, 1024u) : sdesc(bl + 32u * kk, 16u, 1024u);
+    mma_bf16(d, ad, dh, id, kk > 0 ? 1u : 0u);
+    mma_bf16(d, ad, dl, id, 1u);
+  }
+}
+
+// Same with A = hi (ah) + lo (al): hi*hi + hi*lo + lo*hi (12 MMAs)
+template <bool kBMN>
+__device__ __forceinline__ void issue_rowout3(uint32_t d, uint32_t ah, uint32_t al, uint32_t bh,
+                                              uint32_t bl) {
+  const uint32_t id = idesc_bf16(128, 64, false, kBMN);
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const uint64_t adh = sdesc(ah + 32u * kk, 16u, 1024u), adl = sdesc(al + 32u * kk, 16u, 1024u);
+    const uint64_t dh = kBMN ? sdesc(bh + 2048u * kk, kTile, 1024u) : sdesc(bh + 32u * kk, 16u, 1024u);
+    const uint64_t dl = kBMN ? sdesc(bl + 2048u * kk, kTile, 1024u) : sdesc(bl + 32u * kk, 16u, 1024u);
+    mma_bf16(d, adh, dh, id, kk > 0 ? 1u : 0u);
+    mma_bf16(d, adh, dl, id, 1u);
+    mma_bf16(d, adl, dh, id, 1u);
+  }
+}
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, float v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr),
+               "r"(__float_as_uint(v))
+               : "memory");
+}
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __uint_as_float(v);
+}
+
+// ---- setup / mask warp ----------------------------------------------------------
+__device__ __forceinline__ uint32_t setup(uint8_t* smem, Bars* br, uint32_t* tslot, int warp) {
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&br->raw_full[i], 1);
+      mbar_init(&br->slot_free[i], 1);
+      mbar_init(&br->split_full[i], 4);
+      mbar_init(&br->mma_done[i], 1);
+      mbar_init(&br->staged[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&br->fl_full[i], 1);
+      mbar_init(&br->fl_empty[i], 8);
+    }
+    mbar_init(&br->op_ready, 1);
+    mbar_init(&br->acc_free, 4);
+    mbar_init(&br->red_done, 1);
+    d32::fence_barrier_init();
+  }
+  if (warp == kWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_u32(tslot)), "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  return *tslot;
+}
+__device__ __forceinline__ void teardown(uint32_t tmem, int warp) {
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpMma) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  }
+}
+__device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars* br, int lane) {
+  UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
+  const int units = (int)(p.B * p.H), H = (int)p.H;
+  int j = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+    const int sl = j & 1;
+    mbar_wait(&br->fl_empty[sl], ((j >> 1) & 1) ^ 1);
+    tc::mask_unit(p, u / H, reinterpret_cast<uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8)),
+                  &ucs[sl], lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&br->fl_full[sl]);
+  }
+}
+// The M = 64 accumulator row of this thread (lanes 0-15 of each warp hold
+// rows 16 wq + lane), plus the flushed running sum; `valid` = lane < 16.
+__device__ __forceinline__ void acc_row(uint32_t tmem, const float* run, int wq, int lane,
+                                        bool with_run, float (&r)[64]) {
+  tmem_ld64(tmem + ((uint32_t)(32 * wq) << 16), r);
+  if (with_run && lane < 16) {
+    const float4* rr = reinterpret_cast<const float4*>(run + (16 * wq + lane) * 64);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float4 v = rr[k];
+      r[4 * k] += v.x;
+      r[4 * k + 1] += v.y;
+      r[4 * k + 2] += v.z;
+      r[4 * k + 3] += v.w;
+    }
+  }
+}
+__device__ __forceinline__ void flush_acc(uint32_t tmem, float* run, int wq, int lane, bool first) {
+  float r[64];
+  acc_row(tmem, run, wq, lane, !first, r);
+  if (lane < 16) {
+    float4* rr = reinterpret_cast<float4*>(run + (16 * wq + lane) * 64);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) rr[k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+  }
+}
+__device__ __forceinline__ void arrive_staged(Bars* br, int b, int lane) {
+  fence_proxy_async();
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&br->staged[b]);
+}
+
+// ======================================================================================
+// Forward
+// ======================================================================================
+__global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
+    const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
+    const OpParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int N = (int)p.N, H = (int)p.H;
+  const int units = (int)(p.B * p.H);
+  const int C = (N + kRows - 1) / kRows;
+  const int P = (p.out != nullptr || p.saved_norms != nullptr) ? 2 : 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
+  UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
+  uint8_t* ops = smem + kOffOps;
+  float* run = reinterpret_cast<float*>(smem + kOffRun);
+  const uint32_t tmem = setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
+  tc::pdl_wait();
+  const KernelStamp stamp_(p);
+  tc::pdl_launch_dependents();
+
+  if (warp == kWarpProducer) {
+    if (lane == 0) {
+      d32::prefetch_map(&tk);
+      d32::prefetch_map(&tv);
+      d32::prefetch_map(&tq);
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int ps = 0; ps < P; ++ps)
+          for (int c = 0; c < C; ++c, ++it) {
+            const int st = slot3(it);
+            mbar_wait(&br->slot_free[st], par3(it) ^ 1u);
+            uint8_t* X = smem + kOffRing + st * kSlot;
+            if (ps == 0) {
+              mbar_expect_tx(&br->raw_full[st], 2 * kTile);
+              tma_load_4d(X, &tk, 0, c * kRows, h, b, &br->raw_full[st]);
+              tma_load_4d(X + kTile, &tv, 0, c * kRows, h, b, &br->raw_full[st]);
+            } else {
+              mbar_expect_tx(&br->raw_full[st], kTile);
+              tma_load_4d(X, &tq, 0, c * kRows, h, b, &br->raw_full[st]);
+            }
+          }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    int it = 0, j = 0, nflush = 0;
+    const uint32_t base = smem_u32(smem);
+    const uint32_t opS = base + kOffOps;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      for (int ps = 0; ps < P; ++ps)
+        for (int c = 0; c < C; ++c, ++it) {
+          const int st = slot3(it);
+          mbar_wait(&br->split_full[st], par3(it));
+          if (ps == 0 && c == 0 && P == 1 && j > 0) mbar_wait(&br->op_ready, (j - 1) & 1);
+          if (ps == 0 && c > 0 && c % kFlush == 0) mbar_wait(&br->acc_free, (nflush++) & 1);
+          if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
+          tc_fence_after();
+          const uint32_t X = base + kOffRing + st * kSlot, Z = X + 2 * kTile;
+          if (elect_one()) {
+            if (ps == 0) {  // S += K~^T V (attention.cpp:345-353), K~ = hi (Z) + lo (X)
+              const int ks = (min(kRows, N - c * kRows) + 15) >> 4;
+              issue_reduction(tmem, Z, X + kTile, ks, c % kFlush == 0);
+              issue_reduction(tmem, X, X + kTile, ks, false);
+            } else {  // O = Q~ S (:379-387)
+              issue_rowout3<true>(tmem + kBuf0 + kBufCols * st, Z, X, opS, opS + kStateTile);
+            }
+            mma_commit(&br->mma_done[st]);
+          }
+          __syncwarp();
+        }
+    }
+  } else if (warp == kWarpMask) {
+    mask_loop(p, smem, br, lane);
+  } else if (warp == kWarpStore) {
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int ps = 0; ps < P; ++ps)
+          for (int c = 0; c < C; ++c, ++it) {
+            const int st = slot3(it);
+            mbar_wait(&br->staged[st], par3(it));
+            if (ps == 1 && p.out) {
+              tma_store_4d(&to, smem + kOffRing + st * kSlot + 2 * kTile, 0, c * kRows, h, b);
+              bulk_wait_read0();
+            }
+            mbar_arrive(&br->slot_free[st]);
+          }
+      }
+      bulk_wait0();
+    }
+  } else {
+    const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
+    const float eps = (float)p.eps;
+    float* norms_all = static_cast<float*>(p.saved_norms);
+    float* gS_all = static_cast<float*>(p.saved_S);
+    const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
+    int it = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int sl = j & 1;
+      const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
+      float* norms = norms_all ? norms_all + (int64_t)u * 2 * N : nullptr;
+      mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
+      const UnitConst uc = ucs[sl];
+      for (int k = 0; k < P * C; ++k, ++it) {
+        const int ps = k >= C, c = ps ? k - C : k;
+        const int st = slot3(it);
+        const int r = c * kRows + t;
+        uint8_t* X = smem + kOffRing + st * kSlot;
+        uint8_t* Z = X + 2 * kTile;
+        if (g == 0) {  // ---------------- splitter ----------------
+          mbar_wait(&br->raw_full[st], par3(it));
+          float x[64];
+          load_row(X, t, x);
+          const float ss = sumsq64(x) + eps;
+          const float iv = rsqrtf(ss);
+          if (ps == 0) {  // k~ masked (attention.cpp:334-343)
+            const bool f = r < N && tc::flag_at(fl, r);
+            if (norms && r < N) norms[N + r] = f ? ss * iv : 1.0f;
+            const float sc = f ? iv : 0.f;
+#pragma unroll
+            for (int e = 0; e < 64; ++e) x[e] = f ? x[e] * sc : 0.f;  // NaN-safe zeros
+          } else {  // q~ every row (:366-377)
+            if (norms && r < N) norms[r] = ss * iv;
+#pragma unroll
+            for (int e = 0; e < 64; ++e) x[e] *= iv;
+          }
+          store_split_row(Z, X, t, x);  // lo over the raw row (read above, this thread's own)
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&br->split_full[st]);
+        } else {  // ---------------- epiloguer ----------------
+          mbar_wait(&br->mma_done[st], par3(it));
+          tc_fence_after();
+          if (ps == 0) {
+            if (c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
+              flush_acc(tmem, run, wq, lane, c == kFlush - 1);
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&br->acc_free);
+            }
+            if (c == C - 1) {  // S complete: saved S + the bf16 hi/lo state operand
+              float s[64];
+              acc_row(tmem, run, wq, lane, C > kFlush, s);
+              if (lane < 16) {
+                const int a = 16 * wq + lane;
+                if (gS_all) {
+                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 4096 + a * 64);
+#pragma unroll
+                  for (int e = 0; e < 16; ++e)
+                    gs[e] = make_float4(s[4 * e], s[4 * e + 1], s[4 * e + 2], s[4 * e + 3]);
+                }
+                store_state_row(ops, ops + kStateTile, a, s);
+              }
+              fence_proxy_async();
+              tc_fence_before();
+              tc::group_sync(g);
+              if (t == 0) mbar_arrive(&br->op_ready);
+            }
+          } else {  // O rows = s (Q~ S), staged in Z (its MMAs are done)
+            float o[64];
+            tmem_ld64(tmem + kBuf0 + kBufCols * st + lane_base, o);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) o[e] *= uc.s;
+            store_row(Z, t, o);
+          }
+          arrive_staged(br, st, lane);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
+    }
+  }
+  teardown(tmem, warp);
+}
+
+// ======================================================================================
+// Backward
+// ======================================================================================
+__global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
+    const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+    const __grid_constant__ CUtensorMap tdq, const __grid_constant__ CUtensorMap tdk,
+    const __grid_constant__ CUtensorMap tdv, const OpParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int N = (int)p.N, H = (int)p.H;
+  const int units = (int)(p.B * p.H);
+  const int C = (N + kRows - 1) / kRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
+  UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
+  double* dm_x = reinterpret_cast<double*>(smem + kOffMisc + 40);
+  uint8_t* ops = smem + kOffOps;
+  float* run = reinterpret_cast<float*>(smem + kOffRun);
+  const uint32_t tmem = setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
+  tc::pdl_wait();
+  const KernelStamp stamp_(p);
+  tc::pdl_launch_dependents();
+
+  if (warp == kWarpProducer) {
+    if (lane == 0) {
+      d32::prefetch_map(&tq);
+      d32::prefetch_map(&tdo);
+      d32::prefetch_map(&tk);
+      d32::prefetch_map(&tv);
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int ps = 0; ps < 2; ++ps)
+          for (int c = 0; c < C; ++c, ++it) {
+            const int st = slot3(it);
+            mbar_wait(&br->slot_free[st], par3(it) ^ 1u);
+            uint8_t* X = smem + kOffRing + st * kSlot;
+            mbar_expect_tx(&br->raw_full[st], 2 * kTile);
+            tma_load_4d(X, ps == 0 ? &tq : &tk, 0, c * kRows, h, b, &br->raw_full[st]);
+            tma_load_4d(X + kTile, ps == 0 ? &tdo : &tv, 0, c * kRows, h, b, &br->raw_full[st]);
+          }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    int it = 0, j = 0, nflush = 0;
+    const uint32_t base = smem_u32(smem);
+    const uint32_t opS = base + kOffOps, opA = opS + 2 * kStateTile;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      for (int ps = 0; ps < 2; ++ps)
+        for (int c = 0; c < C; ++c, ++it) {
+          const int st = slot3(it);
+          mbar_wait(&br->split_full[st], par3(it));
+          if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
+          if (ps == 0 && c > 0 && c % kFlush == 0) mbar_wait(&br->acc_free, (nflush++) & 1);
+          tc_fence_after();
+          const uint32_t X = base + kOffRing + st * kSlot, Y = X + kTile, Z = X + 2 * kTile;
+          const uint32_t D = tmem + kBuf0 + kBufCols * st;
+          if (elect_one()) {
+            if (ps == 0) {
+              // G += Q~^T dO (attention.cpp:405)
+              const int rows = min(kRows, N - c * kRows);
+              issue_reduction(tmem, Z, Y, (rows + 15) >> 4, c % kFlush == 0);
+              issue_reduction(tmem, X, Y, (rows + 15) >> 4, false);
+              // dQ~ (unscaled) = dO S^T (:410-411): A = dO (K-major), B row n = S row n
+              issue_rowout<false>(D, Y, opS, opS + kStateTile);
+              // G complete (and every MMA that reads this unit's S rows: the
+              // splitter may overwrite them once the G-epilogue has run)
+              if (c == C - 1) mma_commit(&br->red_done);
+            } else {
+              issue_rowout3<true>(D, Z, X, opA, opA + kStateTile);     // dV = K~ dA (:416)
+              issue_rowout<false>(D + 64, Y, opA, opA + kStateTile);   // dK~ = V dA^T (:415)
+            }
+            mma_commit(&br->mma_done[st]);
+          }
+          __syncwarp();
+        }
+    }
+  } else if (warp == kWarpMask) {
+    mask_loop(p, smem, br, lane);
+  } else if (warp == kWarpStore) {
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / H, h = u - b * H;
+        for (int ps = 0; ps < 2; ++ps)
+          for (int c = 0; c < C; ++c, ++it) {
+            const int st = slot3(it);
+            uint8_t* X = smem + kOffRing + st * kSlot;
+            mbar_wait(&br->staged[st], par3(it));
+            if (ps == 0) {
+              tma_store_4d(&tdq, X + 2 * kTile, 0, c * kRows, h, b);
+            } else {
+              tma_store_4d(&tdv, X + 2 * kTile, 0, c * kRows, h, b);
+              tma_store_4d(&tdk, X + kTile, 0, c * kRows, h, b);
+            }
+            bulk_wait_read0();
+            mbar_arrive(&br->slot_free[st]);
+          }
+      }
+      bulk_wait0();
+    }
+  } else {
+    const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
+    const float eps = (float)p.eps;
+    const float* gS_all = static_cast<const float*>(p.saved_S);
+    const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
+    const float qnan = __int_as_float(0x7fc00000);
+    int it = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int sl = j & 1;
+      const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
+      mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
+      const UnitConst uc = ucs[sl];
+      for (int k = 0; k < 2 * C; ++k, ++it) {
+        const int ps = k >= C, c = ps ? k - C : k;
+        const int st = slot3(it);
+        const int r = c * kRows + t;
+        uint8_t* X = smem + kOffRing + st * kSlot;
+        uint8_t* Y = X + kTile;
+        uint8_t* Z = X + 2 * kTile;
+        const uint32_t D = tmem + kBuf0 + kBufCols * st + lane_base;
+        if (g == 0) {  // ---------------- splitter ----------------
+          if (ps == 0 && c == 0) {
+            // this unit's S (saved by the forward) as bf16 hi / lo rows; the previous
+            // unit's dQ~ MMAs and G-epilogue (dm) have read its S (op_ready)
+            if (j > 0) mbar_wait(&br->op_ready, (j - 1) & 1);
+            const int a = t >> 1, hf = t & 1;
+            const float4* gs = reinterpret_cast<const float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 32 * hf);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // granules 4hf + q of row a: 8 values each
+              const float4 v0 = __ldg(gs + 2 * q), v1 = __ldg(gs + 2 * q + 1);
+              const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+              float hi[8], lo[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                hi[e] = __bfloat162float(__float2bfloat16_rn(vv[e]));
+                lo[e] = vv[e] - hi[e];
+              }
+              const uint32_t o = goff(a, 4 * hf + q);
+              *reinterpret_cast<uint4*>(ops + o) =
+                  make_uint4(pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]), pack2(hi[6], hi[7]));
+              *reinterpret_cast<uint4*>(ops + kStateTile + o) =
+                  make_uint4(pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]), pack2(lo[6], lo[7]));
+            }
+          }
+          mbar_wait(&br->raw_full[st], par3(it));
+          float x[64];
+          load_row(X, t, x);
+          const float iv = rsqrtf(sumsq64(x) + eps);
+          if (ps == 0) {  // q~ (rows past N: exact zeros in G even for eps = 0)
+            const float sc = r < N ? iv : 0.f;
+#pragma unroll
+            for (int e = 0; e < 64; ++e) x[e] *= sc;
+          } else {  // k~ masked (padded rows never multiplied in)
+            const bool f = r < N && tc::flag_at(fl, r);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) x[e] = f ? x[e] * iv : 0.f;
+          }
+          store_split_row(Z, X, t, x);
+          tmem_st1(tmem + kInv + st + lane_base, iv);  // 1/norm for the epiloguer's Jacobian
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&br->split_full[st]);
+        } else {  // ---------------- epiloguer ----------------
+          if (ps == 0 && c == C - 1) {
+            // G complete: dm = -ln(n) s <G, S> (:408), dA = s G (:412-413)
+            mbar_wait(&br->red_done, j & 1);
+            tc_fence_after();
+            float gr[64];
+            acc_row(tmem, run, wq, lane, C > kFlush, gr);
+            double dot = 0.0;
+            if (lane < 16) {
+              const int a = 16 * wq + lane;
+              dot = (double)dot_state_row(ops, ops + kStateTile, a, gr);
+#pragma unroll
+              for (int e = 0; e < 64; ++e) gr[e] *= uc.s;
+              store_state_row(ops + 2 * kStateTile, ops + 3 * kStateTile, a, gr);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+            if (lane == 0) dm_x[wq] = dot;
+            fence_proxy_async();
+            tc_fence_before();
+            tc::group_sync(g);
+            if (t == 0) {
+              const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
+              if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
+              mbar_arrive(&br->op_ready);
+            }
+          }
+          mbar_wait(&br->mma_done[st], par3(it));
+          tc_fence_after();
+          if (ps == 0 && c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush G
+            flush_acc(tmem, run, wq, lane, c == kFlush - 1);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&br->acc_free);
+          }
+          float x[64], gv[64];
+          load_split_row(Z, X, t, x);  // q~ / k~ = hi + lo in fp32 for the Jacobian
+          const float iv = tmem_ld1(tmem + kInv + st + lane_base);
+          if (ps == 0) {
+            // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428)
+            tmem_ld64(D, gv);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) gv[e] *= uc.s;
+            const float pr = dot64(gv, x);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) gv[e] = (gv[e] - pr * x[e]) * iv;
+            store_row(Z, t, gv);
+          } else {
+            const bool f = r < N && tc::flag_at(fl, r);
+            const bool nan_out = uc.tn == 0;
+            // dK_i = v_i ? (g - (g.k~)k~) / nk : 0 (:430-437), staged in Y (V is done)
+            tmem_ld64(D + 64, gv);
+            const float pr = dot64(gv, x);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) gv[e] = nan_out ? qnan : (f ? (gv[e] - pr * x[e]) * iv : 0.f);
+            store_row(Y, t, gv);
+            // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439), staged in Z (K~ is done)
+            tmem_ld64(D, gv);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) gv[e] = nan_out ? qnan : (f ? gv[e] : 0.f);
+            store_row(Z, t, gv);
+          }
+          arrive_staged(br, st, lane);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
+    }
+  }
+  if (threadIdx.x == 128 && p.dm_total) __threadfence();
+  teardown(tmem, warp);
+  if (p.dm_total) tc::last_cta_dm_total(p, units, smem + kOffRing);
+}
+
+}  // namespace tcb
+
+// ---- host side ----------------------------------------------------------------------
+
+// 4-D bf16 map over (D, N, H, B), box (64, 128, 1, 1), 128-byte swizzle.
+inline bool make_bf16_chunk_map(CUtensorMap* map, const void* base, const OpParams& p) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)p.N, (cuuint64_t)p.H, (cuuint64_t)p.B};
+  cuuint64_t strides[3] = {(cuuint64_t)p.sn * 2, (cuuint64_t)p.sh * 2, (cuuint64_t)p.sb * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)tcb::kRows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline bool tcb_layout_ok(const OpParams& p, std::initializer_list<const void*> ptrs) {
+  if (p.D != 64 || p.N < 1 || p.N > tcb::kMaxN) return false;
+  if ((p.sn * 2) % 16 || (p.sh * 2) % 16 || (p.sb * 2) % 16) return false;
+  if (p.B * p.H > (1ll << 31) - 1) return false;
+  for (const void* q : ptrs)
+    if (q && (reinterpret_cast<uintptr_t>(q) & 15)) return false;
+  return encode_fn() != nullptr && getenv("COTTEN_NO_TCB") == nullptr;
+}
+template <typename T>
+inline bool tcb_fwd_supported(const OpParams& p) {
+  if constexpr (!std::is_same<T, __nv_bfloat16>::value) {
+    return false;
+  } else {
+    return tcb_layout_ok(p, {p.q, p.k, p.v, p.out});
+  }
+}
+template <typename T>
+inline bool tcb_bwd_supported(const OpParams& p) {
+  if constexpr (!std::is_same<T, __nv_bfloat16>::value) {
+    return false;
+  } else {
+    return p.saved_S != nullptr && tcb_layout_ok(p, {p.q, p.k, p.v, p.dout, p.dq, p.dk, p.dv});
+  }
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_tcb_pdl(void (*kern)(KArgs...), int grid, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tcb::kThreads);
+  cfg.dynamicSmemBytes = tcb::kSmemBytes;
+  cfg.stream = st;
+  static const bool pdl = getenv("COTTEN_NO_PDL") == nullptr;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+inline int launch_tcb_fwd(const OpParams& p, cudaStream_t st) {
+  CUtensorMap mq, mk, mv, mo;
+  if (!make_bf16_chunk_map(&mq, p.q, p) || !make_bf16_chunk_map(&mk, p.k, p) ||
+      !make_bf16_chunk_map(&mv, p.v, p) || !make_bf16_chunk_map(&mo, p.out ? p.out : p.q, p))
+    return -1;
+  if (cudaFuncSetAttribute(tcb::cos_fwd_tcb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tcb::kSmemBytes) != cudaSuccess)
+    return -1;
+  const int grid = std::min((int)(p.B * p.H), sm_count());
+  if (launch_tcb_pdl(tcb::cos_fwd_tcb_kernel, grid, st, mq, mk, mv, mo, p) != cudaSuccess) return -1;
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+inline int launch_tcb_bwd(const OpParams& p, cudaStream_t st) {
+  CUtensorMap mq, mk, mv, mg, mdq, mdk, mdv;
+  if (!make_bf16_chunk_map(&mq, p.q, p) || !make_bf16_chunk_map(&mk, p.k, p) ||
+      !make_bf16_chunk_map(&mv, p.v, p) || !make_bf16_chunk_map(&mg, p.dout, p) ||
+      !make_bf16_chunk_map(&mdq, p.dq, p) || !make_bf16_chunk_map(&mdk, p.dk, p) ||
+      !make_bf16_chunk_map(&mdv, p.dv, p))
+    return -1;
+  if (cudaFuncSetAttribute(tcb::cos_bwd_tcb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tcb::kSmemBytes) != cudaSuccess)
+    return -1;
+  const int grid = std::min((int)(p.B * p.H), sm_count());
+  if (launch_tcb_pdl(tcb::cos_bwd_tcb_kernel, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, p) !=
+      cudaSuccess)
+    return -1;
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace cotten
