@@ -31,6 +31,7 @@ struct OpParams {
   int64_t sb, sh, sn, msb;
   double m, eps;
   const double* m_dev;    // device-resident m (cotten_*_mdev): read by the kernels instead of m
+  int l2_ahead;           // tcgen05 producers: L2 prefetch distance in items (0 = off)
 };
 
 // The exponent m of s = exp(-m ln true_n): the host value, or the device-resident

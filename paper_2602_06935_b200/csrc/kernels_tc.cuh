@@ -217,6 +217,33 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
       : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// L2 prefetch of one TMA box (no shared memory, no barrier): deepens the load
+// pipeline beyond the 3-slot ring, whose slots stay busy from the load to the
+// store of their chunk.
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2,
+                                                int c3) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// The chunk item `it` of this CTA's persistent schedule (units blockIdx.x +
+// j gridDim.x, each P passes x C chunks): false past the last unit.
+struct ItemPos {
+  int b, h, ps, c;
+};
+__device__ __forceinline__ bool item_pos(int it, int P, int C, int units, int H, ItemPos& o) {
+  const int per = P * C;
+  const int j = it / per, rem = it - j * per;
+  const int u = blockIdx.x + j * gridDim.x;
+  if (u >= units) return false;
+  o.b = u / H;
+  o.h = u - o.b * H;
+  o.ps = rem / C;
+  o.c = rem - o.ps * C;
+  return true;
+}
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -855,6 +882,15 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            ItemPos f;
+            if (p.l2_ahead && item_pos(it + p.l2_ahead, P, C, units, H, f)) {
+              if (f.ps == 0) {
+                tma_prefetch_4d(&tk, 0, f.c * kRows, f.h, f.b);
+                tma_prefetch_4d(&tv, 0, f.c * kRows, f.h, f.b);
+              } else {
+                tma_prefetch_4d(&tq, 0, f.c * kRows, f.h, f.b);
+              }
+            }
             mbar_wait(&br->raw_empty[st], par3(it) ^ 1u);
             uint8_t* dst = smem + kOffRaw + st * kStage;
             if (ps == 0) {
@@ -1064,6 +1100,11 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            ItemPos f;
+            if (p.l2_ahead && item_pos(it + p.l2_ahead, 2, C, units, H, f)) {
+              tma_prefetch_4d(f.ps == 0 ? &tq : &tk, 0, f.c * kRows, f.h, f.b);
+              tma_prefetch_4d(f.ps == 0 ? &tdo : &tv, 0, f.c * kRows, f.h, f.b);
+            }
             mbar_wait(&br->raw_empty[st], par3(it) ^ 1u);
             uint8_t* dst = smem + kOffRaw + st * kStage;
             mbar_expect_tx(&br->raw_full[st], 2 * kTile);
@@ -1456,6 +1497,16 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, cudaStream_t st,
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// L2 prefetch distance of the tcgen05 producers (items); COTTEN_L2_AHEAD
+// overrides it (0 = off) for A/B runs.
+inline int l2_ahead_items() {
+  static const int v = [] {
+    const char* e = getenv("COTTEN_L2_AHEAD");
+    return e ? atoi(e) : 0;  // off: measured neutral-to-negative
+  }();
+  return v;
+}
+
 inline int launch_tc_fwd(const OpParams& p, cudaStream_t st) {
   CUtensorMap mq, mk, mv, mo;
   if (!make_chunk_map(&mq, p.q, p) || !make_chunk_map(&mk, p.k, p, true) ||
@@ -1467,6 +1518,7 @@ inline int launch_tc_fwd(const OpParams& p, cudaStream_t st) {
     return -1;
   const int grid = std::min(units, sm_count());
   OpParams q = p;
+  q.l2_ahead = l2_ahead_items();
   q.workspace = tc_trace_begin(grid);
   if (launch_pdl(tc::cos_fwd_tc_kernel, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
   tc_trace_end(q.workspace, grid, "fwd", st);
@@ -1486,6 +1538,7 @@ inline int launch_tc_bwd(const OpParams& p, cudaStream_t st) {
     return -1;
   const int grid = std::min(units, sm_count());
   OpParams q = p;
+  q.l2_ahead = l2_ahead_items();
   q.workspace = tc_trace_begin(grid);
   if (launch_pdl(tc::cos_bwd_tc_kernel, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, q) != cudaSuccess)
     return -1;

@@ -31,9 +31,11 @@
 // MN-major B of O = Q~ S / dV = K~ dA and the K-major B of dQ~ = dO S^T /
 // dK~ = V dA^T alike.
 //
-// Warp roles (384 threads): 0-3 splitter (thread t = chunk row t), 4-7
-// epiloguer (thread t = TMEM lane t), 8 TMA producer, 9 MMA issuer, 10 mask
-// warp, 11 store warp (TMA stores, then frees the whole slot).
+// Warp roles (512 threads): 0-7 splitter (two threads per chunk row, 32
+// columns each: a single splitter warp per SMSP was the latency-bound stage,
+// measured), 8-11 epiloguer (thread t = TMEM lane t, rows processed in two
+// 32-column halves to stay within 128 registers), 12 TMA producer, 13 MMA
+// issuer, 14 mask warp, 15 store warp (TMA stores, then frees the slot).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -67,8 +69,10 @@ constexpr uint32_t kTile = 16384;  // 128 rows x 128 B
 constexpr int kRing = 3;
 constexpr int kMaxN = 16384;
 constexpr int kFlush = 4;  // S / G accumulator flushed every 4 chunks (<= 32 MMAs per chain)
-constexpr int kWarpProducer = 8, kWarpMma = 9, kWarpMask = 10, kWarpStore = 11;
-constexpr int kThreads = 12 * 32;
+constexpr int kSplitWarps = 8, kEpiWarps = 4;
+constexpr int kWarpEpi0 = kSplitWarps;
+constexpr int kWarpProducer = 12, kWarpMma = 13, kWarpMask = 14, kWarpStore = 15;
+constexpr int kThreads = 16 * 32;
 
 // shared memory: per slot X, Y (raw TMA tiles) and Z (normalised / staging)
 constexpr uint32_t kSlot = 3 * kTile;
@@ -77,7 +81,8 @@ constexpr uint32_t kStateTile = 64 * 128;  // 64 x 64 bf16 rows
 constexpr uint32_t kOffOps = kOffRing + kRing * kSlot;   // S hi, S lo, dA hi, dA lo
 constexpr uint32_t kOffRun = kOffOps + 4 * kStateTile;   // fp32 running sum, 64 x 64
 constexpr uint32_t kOffFlags = kOffRun + 64 * 64 * 4;    // 2 x 2 KB bitmasks
-constexpr uint32_t kOffMisc = kOffFlags + 2 * (kMaxN / 8);
+constexpr uint32_t kOffInv = kOffFlags + 2 * (kMaxN / 8);  // per slot 128 x 1/norm (bwd)
+constexpr uint32_t kOffMisc = kOffInv + kRing * kRows * 4;
 constexpr uint32_t kOffBar = kOffMisc + 128;
 constexpr uint32_t kSmemBytes = kOffBar + 32 * 8;
 static_assert(kSmemBytes <= 227 * 1024, "shared-memory budget");
@@ -87,7 +92,26 @@ static_assert(kSmemBytes <= 227 * 1024, "shared-memory budget");
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kBuf0 = 64;
 constexpr uint32_t kBufCols = 128;
-constexpr uint32_t kInv = kBuf0 + kRing * kBufCols;  // + slot: the row's 1/norm (bwd)
+
+// Optional per-item trace (-DCOTTEN_TCB_TRACE=1): clock64 stamps of the first
+// kTraceItems items of every CTA into p.workspace [cta][item][8]:
+// 0 splitter waits raw, 1 raw landed, 2 split published, 3 MMA sees split,
+// 4 MMAs issued, 5 epiloguer sees MMAs done, 6 outputs staged, 7 slot freed.
+#ifndef COTTEN_TCB_TRACE
+#define COTTEN_TCB_TRACE 0
+#endif
+constexpr int kTraceItems = 64;
+#if COTTEN_TCB_TRACE
+#define TCB_TRACE(k, cond)                                                                   \
+  do {                                                                                       \
+    if ((cond) && p.workspace && it < kTraceItems)                                           \
+      static_cast<long long*>(p.workspace)[(blockIdx.x * kTraceItems + it) * 8 + (k)] = clock64(); \
+  } while (0)
+#else
+#define TCB_TRACE(k, cond) \
+  do {                     \
+  } while (0)
+#endif
 
 __device__ __forceinline__ int slot3(int it) { return it % kRing; }
 __device__ __forceinline__ uint32_t par3(int it) { return (uint32_t)(it / kRing) & 1u; }
@@ -103,68 +127,61 @@ static_assert(sizeof(Bars) <= 256, "barrier area");
 __device__ __forceinline__ uint32_t goff(int row, int j) {
   return (uint32_t)row * 128u + ((uint32_t)(j ^ (row & 7)) << 4);
 }
-__device__ __forceinline__ void load_row(const uint8_t* tile, int row, float (&x)[64]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint4 v = *reinterpret_cast<const uint4*>(tile + goff(row, j));
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-      x[8 * j + 2 * e] = f.x;
-      x[8 * j + 2 * e + 1] = f.y;
-    }
-  }
-}
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
-__device__ __forceinline__ void store_row(uint8_t* tile, int row, const float (&x)[64]) {
+__device__ __forceinline__ void unpack8(const uint4 v, float* x) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
-    *reinterpret_cast<uint4*>(tile + goff(row, j)) =
-        make_uint4(pack2(x[8 * j], x[8 * j + 1]), pack2(x[8 * j + 2], x[8 * j + 3]),
-                   pack2(x[8 * j + 4], x[8 * j + 5]), pack2(x[8 * j + 6], x[8 * j + 7]));
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+    x[2 * e] = f.x;
+    x[2 * e + 1] = f.y;
+  }
 }
-// x = hi + lo as two bf16 rows: hi into `hi_tile`, lo into `lo_tile`
-__device__ __forceinline__ void store_split_row(uint8_t* hi_tile, uint8_t* lo_tile, int row,
-                                                const float (&x)[64]) {
+__device__ __forceinline__ uint4 pack8(const float* x) {
+  return make_uint4(pack2(x[0], x[1]), pack2(x[2], x[3]), pack2(x[4], x[5]), pack2(x[6], x[7]));
+}
+// columns [32 h, 32 h + 32) of a row = granules 4h .. 4h + 3
+__device__ __forceinline__ void load_half(const uint8_t* tile, int row, int h, float (&x)[32]) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float h[8], l[8];
+  for (int q = 0; q < 4; ++q) unpack8(*reinterpret_cast<const uint4*>(tile + goff(row, 4 * h + q)), x + 8 * q);
+}
+__device__ __forceinline__ void store_half(uint8_t* tile, int row, int h, const float (&x)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(tile + goff(row, 4 * h + q)) = pack8(x + 8 * q);
+}
+// x = hi + lo (bf16 each) for half h of a row
+__device__ __forceinline__ void store_split_half(uint8_t* hi_tile, uint8_t* lo_tile, int row, int h,
+                                                 const float (&x)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float hi[8], lo[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      h[e] = __bfloat162float(__float2bfloat16_rn(x[8 * j + e]));
-      l[e] = x[8 * j + e] - h[e];
+      hi[e] = __bfloat162float(__float2bfloat16_rn(x[8 * q + e]));
+      lo[e] = x[8 * q + e] - hi[e];
     }
-    *reinterpret_cast<uint4*>(hi_tile + goff(row, j)) =
-        make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7]));
-    *reinterpret_cast<uint4*>(lo_tile + goff(row, j)) =
-        make_uint4(pack2(l[0], l[1]), pack2(l[2], l[3]), pack2(l[4], l[5]), pack2(l[6], l[7]));
+    *reinterpret_cast<uint4*>(hi_tile + goff(row, 4 * h + q)) = pack8(hi);
+    *reinterpret_cast<uint4*>(lo_tile + goff(row, 4 * h + q)) = pack8(lo);
   }
 }
-// hi + lo rows back to fp32
-__device__ __forceinline__ void load_split_row(const uint8_t* hi_tile, const uint8_t* lo_tile,
-                                               int row, float (&x)[64]) {
+__device__ __forceinline__ void load_split_half(const uint8_t* hi_tile, const uint8_t* lo_tile,
+                                                int row, int h, float (&x)[32]) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint4 vh = *reinterpret_cast<const uint4*>(hi_tile + goff(row, j));
-    const uint4 vl = *reinterpret_cast<const uint4*>(lo_tile + goff(row, j));
-    const uint32_t wh[4] = {vh.x, vh.y, vh.z, vh.w}, wl[4] = {vl.x, vl.y, vl.z, vl.w};
+  for (int q = 0; q < 4; ++q) {
+    float a[8], b[8];
+    unpack8(*reinterpret_cast<const uint4*>(hi_tile + goff(row, 4 * h + q)), a);
+    unpack8(*reinterpret_cast<const uint4*>(lo_tile + goff(row, 4 * h + q)), b);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 fh = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wh[e]));
-      const float2 fl = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wl[e]));
-      x[8 * j + 2 * e] = fh.x + fl.x;
-      x[8 * j + 2 * e + 1] = fh.y + fl.y;
-    }
+    for (int e = 0; e < 8; ++e) x[8 * q + e] = a[e] + b[e];
   }
 }
-__device__ __forceinline__ float sumsq64(const float (&x)[64]) {
+__device__ __forceinline__ float sumsq32(const float (&x)[32]) {
   float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
 #pragma unroll
-  for (int k = 0; k < 64; k += 4) {
+  for (int k = 0; k < 32; k += 4) {
     a = fmaf(x[k], x[k], a);
     b = fmaf(x[k + 1], x[k + 1], b);
     c = fmaf(x[k + 2], x[k + 2], c);
@@ -172,10 +189,10 @@ __device__ __forceinline__ float sumsq64(const float (&x)[64]) {
   }
   return (a + b) + (c + d);
 }
-__device__ __forceinline__ float dot64(const float (&x)[64], const float (&y)[64]) {
+__device__ __forceinline__ float dot32(const float (&x)[32], const float (&y)[32]) {
   float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
 #pragma unroll
-  for (int k = 0; k < 64; k += 4) {
+  for (int k = 0; k < 32; k += 4) {
     a = fmaf(x[k], y[k], a);
     b = fmaf(x[k + 1], y[k + 1], b);
     c = fmaf(x[k + 2], y[k + 2], c);
@@ -183,48 +200,10 @@ __device__ __forceinline__ float dot64(const float (&x)[64], const float (&y)[64
   }
   return (a + b) + (c + d);
 }
-// 64 accumulator columns of this thread's lane
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&r)[64]) {
-  float* a = r;
-  tmem_ld32(taddr, *reinterpret_cast<float(*)[32]>(a));
-  tmem_ld32(taddr + 32, *reinterpret_cast<float(*)[32]>(a + 32));
+// 32 accumulator columns of this thread's lane
+__device__ __forceinline__ void tmem_ld_half(uint32_t taddr, float (&r)[32]) {
+  tmem_ld32(taddr, r);
   tmem_wait_ld();
-}
-// Row a of a 64 x 64 state matrix as bf16 hi / lo rows (x = hi + lo).
-__device__ __forceinline__ void store_state_row(uint8_t* hi, uint8_t* lo, int a,
-                                                const float (&x)[64]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float h[8], l[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      h[e] = __bfloat162float(__float2bfloat16_rn(x[8 * j + e]));
-      l[e] = x[8 * j + e] - h[e];
-    }
-    *reinterpret_cast<uint4*>(hi + goff(a, j)) =
-        make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7]));
-    *reinterpret_cast<uint4*>(lo + goff(a, j)) =
-        make_uint4(pack2(l[0], l[1]), pack2(l[2], l[3]), pack2(l[4], l[5]), pack2(l[6], l[7]));
-  }
-}
-// <x, hi + lo> for row a of a state tile pair, one granule at a time
-__device__ __forceinline__ float dot_state_row(const uint8_t* hi, const uint8_t* lo, int a,
-                                               const float (&x)[64]) {
-  float d0 = 0.f, d1 = 0.f;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint4 vh = *reinterpret_cast<const uint4*>(hi + goff(a, j));
-    const uint4 vl = *reinterpret_cast<const uint4*>(lo + goff(a, j));
-    const uint32_t wh[4] = {vh.x, vh.y, vh.z, vh.w}, wl[4] = {vl.x, vl.y, vl.z, vl.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 fh = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wh[e]));
-      const float2 fl = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wl[e]));
-      d0 = fmaf(x[8 * j + 2 * e], fh.x + fl.x, d0);
-      d1 = fmaf(x[8 * j + 2 * e + 1], fh.y + fl.y, d1);
-    }
-  }
-  return d0 + d1;
 }
 
 // ---- MMA issue ------------------------------------------------------------------
@@ -284,18 +263,6 @@ __device__ __forceinline__ void issue_rowout3(uint32_t d, uint32_t ah, uint32_t 
     mma_bf16(d, adl, dh, id, 1u);
   }
 }
-__device__ __forceinline__ void tmem_st1(uint32_t taddr, float v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr),
-               "r"(__float_as_uint(v))
-               : "memory");
-}
-__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
-  uint32_t v;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-  return __uint_as_float(v);
-}
-
 // ---- setup / mask warp ----------------------------------------------------------
 __device__ __forceinline__ uint32_t setup(uint8_t* smem, Bars* br, uint32_t* tslot, int warp) {
   if (threadIdx.x == 0) {
@@ -303,16 +270,16 @@ __device__ __forceinline__ uint32_t setup(uint8_t* smem, Bars* br, uint32_t* tsl
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&br->raw_full[i], 1);
       mbar_init(&br->slot_free[i], 1);
-      mbar_init(&br->split_full[i], 4);
+      mbar_init(&br->split_full[i], kSplitWarps);
       mbar_init(&br->mma_done[i], 1);
-      mbar_init(&br->staged[i], 4);
+      mbar_init(&br->staged[i], kEpiWarps);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&br->fl_full[i], 1);
-      mbar_init(&br->fl_empty[i], 8);
+      mbar_init(&br->fl_empty[i], kSplitWarps + kEpiWarps);
     }
     mbar_init(&br->op_ready, 1);
-    mbar_init(&br->acc_free, 4);
+    mbar_init(&br->acc_free, kEpiWarps);
     mbar_init(&br->red_done, 1);
     d32::fence_barrier_init();
   }
@@ -347,16 +314,18 @@ __device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars
     if (lane == 0) mbar_arrive(&br->fl_full[sl]);
   }
 }
-// The M = 64 accumulator row of this thread (lanes 0-15 of each warp hold
-// rows 16 wq + lane), plus the flushed running sum; `valid` = lane < 16.
-__device__ __forceinline__ void acc_row(uint32_t tmem, const float* run, int wq, int lane,
-                                        bool with_run, float (&r)[64]) {
-  tmem_ld64(tmem + ((uint32_t)(32 * wq) << 16), r);
+// Half h of the M = 64 accumulator row of this thread (lanes 0-15 of each
+// warp hold rows 16 wq + lane) plus the flushed running sum.  The running
+// sum's row a = 16 wq + lane keeps float4 k at slot k ^ lane, so the 16
+// lanes of a warp hit 16 different 16-byte slots (2 wavefronts, the minimum).
+__device__ __forceinline__ void acc_half(uint32_t tmem, const float* run, int wq, int lane, int h,
+                                         bool with_run, float (&r)[32]) {
+  tmem_ld_half(tmem + ((uint32_t)(32 * wq) << 16) + 32u * h, r);
   if (with_run && lane < 16) {
     const float4* rr = reinterpret_cast<const float4*>(run + (16 * wq + lane) * 64);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const float4 v = rr[k];
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = rr[(8 * h + k) ^ lane];
       r[4 * k] += v.x;
       r[4 * k + 1] += v.y;
       r[4 * k + 2] += v.z;
@@ -365,19 +334,48 @@ __device__ __forceinline__ void acc_row(uint32_t tmem, const float* run, int wq,
   }
 }
 __device__ __forceinline__ void flush_acc(uint32_t tmem, float* run, int wq, int lane, bool first) {
-  float r[64];
-  acc_row(tmem, run, wq, lane, !first, r);
-  if (lane < 16) {
-    float4* rr = reinterpret_cast<float4*>(run + (16 * wq + lane) * 64);
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    float r[32];
+    acc_half(tmem, run, wq, lane, h, !first, r);
+    if (lane < 16) {
+      float4* rr = reinterpret_cast<float4*>(run + (16 * wq + lane) * 64);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) rr[k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+      for (int k = 0; k < 8; ++k)
+        rr[(8 * h + k) ^ lane] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+    }
   }
+}
+// <x, hi + lo> over half h of row a of a state tile pair
+__device__ __forceinline__ float dot_state_half(const uint8_t* hi, const uint8_t* lo, int a, int h,
+                                                const float (&x)[32]) {
+  float s[32];
+  load_split_half(hi, lo, a, h, s);
+  return dot32(x, s);
 }
 __device__ __forceinline__ void arrive_staged(Bars* br, int b, int lane) {
   fence_proxy_async();
   tc_fence_before();
   __syncwarp();
   if (lane == 0) mbar_arrive(&br->staged[b]);
+}
+__device__ __forceinline__ void epi_sync() {  // the 4 epiloguer warps
+  asm volatile("bar.sync 2, 128;" ::: "memory");
+}
+
+// Splitter: two threads per chunk row; the row's squared norm is the sum of
+// the pair's halves (lanes 2i, 2i + 1 of the same warp).
+struct SplitRow {
+  int row, h;
+  float x[32];
+  float ss;  // |row|^2 (both halves)
+};
+__device__ __forceinline__ void split_load(const uint8_t* X, int t, SplitRow& s) {
+  s.row = t >> 1;
+  s.h = t & 1;
+  load_half(X, s.row, s.h, s.x);
+  const float part = sumsq32(s.x);
+  s.ss = part + __shfl_xor_sync(0xffffffffu, part, 1);
 }
 
 // ======================================================================================
@@ -413,6 +411,15 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            tc::ItemPos f;
+            if (p.l2_ahead && tc::item_pos(it + p.l2_ahead, P, C, units, H, f)) {
+              if (f.ps == 0) {
+                tc::tma_prefetch_4d(&tk, 0, f.c * kRows, f.h, f.b);
+                tc::tma_prefetch_4d(&tv, 0, f.c * kRows, f.h, f.b);
+              } else {
+                tc::tma_prefetch_4d(&tq, 0, f.c * kRows, f.h, f.b);
+              }
+            }
             mbar_wait(&br->slot_free[st], par3(it) ^ 1u);
             uint8_t* X = smem + kOffRing + st * kSlot;
             if (ps == 0) {
@@ -435,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
         for (int c = 0; c < C; ++c, ++it) {
           const int st = slot3(it);
           mbar_wait(&br->split_full[st], par3(it));
+          TCB_TRACE(3, lane == 0);
           if (ps == 0 && c == 0 && P == 1 && j > 0) mbar_wait(&br->op_ready, (j - 1) & 1);
           if (ps == 0 && c > 0 && c % kFlush == 0) mbar_wait(&br->acc_free, (nflush++) & 1);
           if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
@@ -450,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
             }
             mma_commit(&br->mma_done[st]);
           }
+          TCB_TRACE(4, lane == 0);
           __syncwarp();
         }
     }
@@ -469,12 +478,15 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
               bulk_wait_read0();
             }
             mbar_arrive(&br->slot_free[st]);
+            TCB_TRACE(7, true);
           }
       }
       bulk_wait0();
     }
   } else {
-    const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
+    const bool splitter = warp < kWarpEpi0;
+    const int wq = warp & 3;
+    const int t = splitter ? (int)threadIdx.x : (int)threadIdx.x - 32 * kWarpEpi0;
     const float eps = (float)p.eps;
     float* norms_all = static_cast<float*>(p.saved_norms);
     float* gS_all = static_cast<float*>(p.saved_S);
@@ -489,32 +501,34 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
       for (int k = 0; k < P * C; ++k, ++it) {
         const int ps = k >= C, c = ps ? k - C : k;
         const int st = slot3(it);
-        const int r = c * kRows + t;
         uint8_t* X = smem + kOffRing + st * kSlot;
         uint8_t* Z = X + 2 * kTile;
-        if (g == 0) {  // ---------------- splitter ----------------
+        if (splitter) {  // ---------------- splitter (2 threads per row) ----------------
+          TCB_TRACE(0, threadIdx.x == 0);
           mbar_wait(&br->raw_full[st], par3(it));
-          float x[64];
-          load_row(X, t, x);
-          const float ss = sumsq64(x) + eps;
-          const float iv = rsqrtf(ss);
+          TCB_TRACE(1, threadIdx.x == 0);
+          SplitRow s;
+          split_load(X, t, s);
+          const int r = c * kRows + s.row;
+          const float iv = rsqrtf(s.ss + eps);
           if (ps == 0) {  // k~ masked (attention.cpp:334-343)
             const bool f = r < N && tc::flag_at(fl, r);
-            if (norms && r < N) norms[N + r] = f ? ss * iv : 1.0f;
-            const float sc = f ? iv : 0.f;
+            if (norms && r < N && s.h == 0) norms[N + r] = f ? (s.ss + eps) * iv : 1.0f;
 #pragma unroll
-            for (int e = 0; e < 64; ++e) x[e] = f ? x[e] * sc : 0.f;  // NaN-safe zeros
+            for (int e = 0; e < 32; ++e) s.x[e] = f ? s.x[e] * iv : 0.f;  // NaN-safe zeros
           } else {  // q~ every row (:366-377)
-            if (norms && r < N) norms[r] = ss * iv;
+            if (norms && r < N && s.h == 0) norms[r] = (s.ss + eps) * iv;
 #pragma unroll
-            for (int e = 0; e < 64; ++e) x[e] *= iv;
+            for (int e = 0; e < 32; ++e) s.x[e] *= iv;
           }
-          store_split_row(Z, X, t, x);  // lo over the raw row (read above, this thread's own)
+          store_split_half(Z, X, s.row, s.h, s.x);  // lo over this thread's own raw half row
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&br->split_full[st]);
+          TCB_TRACE(2, threadIdx.x == 0);
         } else {  // ---------------- epiloguer ----------------
           mbar_wait(&br->mma_done[st], par3(it));
+          TCB_TRACE(5, t == 0);
           tc_fence_after();
           if (ps == 0) {
             if (c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
@@ -523,32 +537,39 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
               __syncwarp();
               if (lane == 0) mbar_arrive(&br->acc_free);
             }
-            if (c == C - 1) {  // S complete: saved S + the bf16 hi/lo state operand
-              float s[64];
-              acc_row(tmem, run, wq, lane, C > kFlush, s);
-              if (lane < 16) {
-                const int a = 16 * wq + lane;
-                if (gS_all) {
-                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 4096 + a * 64);
+            if (c == C - 1) {  // S complete: saved S + the bf16 hi / lo state operand
+#pragma unroll 1
+              for (int h = 0; h < 2; ++h) {
+                float sv[32];
+                acc_half(tmem, run, wq, lane, h, C > kFlush, sv);
+                if (lane < 16) {
+                  const int a = 16 * wq + lane;
+                  if (gS_all) {
+                    float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 32 * h);
 #pragma unroll
-                  for (int e = 0; e < 16; ++e)
-                    gs[e] = make_float4(s[4 * e], s[4 * e + 1], s[4 * e + 2], s[4 * e + 3]);
+                    for (int e = 0; e < 8; ++e)
+                      gs[e] = make_float4(sv[4 * e], sv[4 * e + 1], sv[4 * e + 2], sv[4 * e + 3]);
+                  }
+                  store_split_half(ops, ops + kStateTile, a, h, sv);
                 }
-                store_state_row(ops, ops + kStateTile, a, s);
               }
               fence_proxy_async();
               tc_fence_before();
-              tc::group_sync(g);
+              epi_sync();
               if (t == 0) mbar_arrive(&br->op_ready);
             }
           } else {  // O rows = s (Q~ S), staged in Z (its MMAs are done)
-            float o[64];
-            tmem_ld64(tmem + kBuf0 + kBufCols * st + lane_base, o);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+              float o[32];
+              tmem_ld_half(tmem + kBuf0 + kBufCols * st + lane_base + 32u * h, o);
 #pragma unroll
-            for (int e = 0; e < 64; ++e) o[e] *= uc.s;
-            store_row(Z, t, o);
+              for (int e = 0; e < 32; ++e) o[e] *= uc.s;
+              store_half(Z, t, h, o);
+            }
           }
           arrive_staged(br, st, lane);
+          TCB_TRACE(6, t == 0);
         }
       }
       __syncwarp();
@@ -576,6 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
   double* dm_x = reinterpret_cast<double*>(smem + kOffMisc + 40);
   uint8_t* ops = smem + kOffOps;
   float* run = reinterpret_cast<float*>(smem + kOffRun);
+  float* invs = reinterpret_cast<float*>(smem + kOffInv);
   const uint32_t tmem = setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
   tc::pdl_wait();
   const KernelStamp stamp_(p);
@@ -593,6 +615,11 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            tc::ItemPos f;
+            if (p.l2_ahead && tc::item_pos(it + p.l2_ahead, 2, C, units, H, f)) {
+              tc::tma_prefetch_4d(f.ps == 0 ? &tq : &tk, 0, f.c * kRows, f.h, f.b);
+              tc::tma_prefetch_4d(f.ps == 0 ? &tdo : &tv, 0, f.c * kRows, f.h, f.b);
+            }
             mbar_wait(&br->slot_free[st], par3(it) ^ 1u);
             uint8_t* X = smem + kOffRing + st * kSlot;
             mbar_expect_tx(&br->raw_full[st], 2 * kTile);
@@ -610,6 +637,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
         for (int c = 0; c < C; ++c, ++it) {
           const int st = slot3(it);
           mbar_wait(&br->split_full[st], par3(it));
+          TCB_TRACE(3, lane == 0);
           if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
           if (ps == 0 && c > 0 && c % kFlush == 0) mbar_wait(&br->acc_free, (nflush++) & 1);
           tc_fence_after();
@@ -617,10 +645,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
           const uint32_t D = tmem + kBuf0 + kBufCols * st;
           if (elect_one()) {
             if (ps == 0) {
-              // G += Q~^T dO (attention.cpp:405)
-              const int rows = min(kRows, N - c * kRows);
-              issue_reduction(tmem, Z, Y, (rows + 15) >> 4, c % kFlush == 0);
-              issue_reduction(tmem, X, Y, (rows + 15) >> 4, false);
+              // G += Q~^T dO (attention.cpp:405), Q~ = hi (Z) + lo (X)
+              const int ks = (min(kRows, N - c * kRows) + 15) >> 4;
+              issue_reduction(tmem, Z, Y, ks, c % kFlush == 0);
+              issue_reduction(tmem, X, Y, ks, false);
               // dQ~ (unscaled) = dO S^T (:410-411): A = dO (K-major), B row n = S row n
               issue_rowout<false>(D, Y, opS, opS + kStateTile);
               // G complete (and every MMA that reads this unit's S rows: the
@@ -632,6 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             }
             mma_commit(&br->mma_done[st]);
           }
+          TCB_TRACE(4, lane == 0);
           __syncwarp();
         }
     }
@@ -655,12 +684,15 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             }
             bulk_wait_read0();
             mbar_arrive(&br->slot_free[st]);
+            TCB_TRACE(7, true);
           }
       }
       bulk_wait0();
     }
   } else {
-    const int g = warp >> 2, wq = warp & 3, t = threadIdx.x & 127;
+    const bool splitter = warp < kWarpEpi0;
+    const int wq = warp & 3;
+    const int t = splitter ? (int)threadIdx.x : (int)threadIdx.x - 32 * kWarpEpi0;
     const float eps = (float)p.eps;
     const float* gS_all = static_cast<const float*>(p.saved_S);
     const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
@@ -674,20 +706,19 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
       for (int k = 0; k < 2 * C; ++k, ++it) {
         const int ps = k >= C, c = ps ? k - C : k;
         const int st = slot3(it);
-        const int r = c * kRows + t;
         uint8_t* X = smem + kOffRing + st * kSlot;
         uint8_t* Y = X + kTile;
         uint8_t* Z = X + 2 * kTile;
-        const uint32_t D = tmem + kBuf0 + kBufCols * st + lane_base;
-        if (g == 0) {  // ---------------- splitter ----------------
+        float* inv_st = invs + st * kRows;
+        if (splitter) {  // ---------------- splitter (2 threads per row) ----------------
           if (ps == 0 && c == 0) {
             // this unit's S (saved by the forward) as bf16 hi / lo rows; the previous
             // unit's dQ~ MMAs and G-epilogue (dm) have read its S (op_ready)
             if (j > 0) mbar_wait(&br->op_ready, (j - 1) & 1);
-            const int a = t >> 1, hf = t & 1;
-            const float4* gs = reinterpret_cast<const float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 32 * hf);
+            const int a = t >> 2, q4 = t & 3;  // row a, granules 2 q4, 2 q4 + 1
+            const float4* gs = reinterpret_cast<const float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 16 * q4);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {  // granules 4hf + q of row a: 8 values each
+            for (int q = 0; q < 2; ++q) {
               const float4 v0 = __ldg(gs + 2 * q), v1 = __ldg(gs + 2 * q + 1);
               const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
               float hi[8], lo[8];
@@ -696,54 +727,58 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
                 hi[e] = __bfloat162float(__float2bfloat16_rn(vv[e]));
                 lo[e] = vv[e] - hi[e];
               }
-              const uint32_t o = goff(a, 4 * hf + q);
-              *reinterpret_cast<uint4*>(ops + o) =
-                  make_uint4(pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]), pack2(hi[6], hi[7]));
-              *reinterpret_cast<uint4*>(ops + kStateTile + o) =
-                  make_uint4(pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]), pack2(lo[6], lo[7]));
+              const uint32_t o = goff(a, 2 * q4 + q);
+              *reinterpret_cast<uint4*>(ops + o) = pack8(hi);
+              *reinterpret_cast<uint4*>(ops + kStateTile + o) = pack8(lo);
             }
           }
+          TCB_TRACE(0, threadIdx.x == 0);
           mbar_wait(&br->raw_full[st], par3(it));
-          float x[64];
-          load_row(X, t, x);
-          const float iv = rsqrtf(sumsq64(x) + eps);
+          TCB_TRACE(1, threadIdx.x == 0);
+          SplitRow s;
+          split_load(X, t, s);
+          const int r = c * kRows + s.row;
+          const float iv = rsqrtf(s.ss + eps);
           if (ps == 0) {  // q~ (rows past N: exact zeros in G even for eps = 0)
             const float sc = r < N ? iv : 0.f;
 #pragma unroll
-            for (int e = 0; e < 64; ++e) x[e] *= sc;
+            for (int e = 0; e < 32; ++e) s.x[e] *= sc;
           } else {  // k~ masked (padded rows never multiplied in)
             const bool f = r < N && tc::flag_at(fl, r);
 #pragma unroll
-            for (int e = 0; e < 64; ++e) x[e] = f ? x[e] * iv : 0.f;
+            for (int e = 0; e < 32; ++e) s.x[e] = f ? s.x[e] * iv : 0.f;
           }
-          store_split_row(Z, X, t, x);
-          tmem_st1(tmem + kInv + st + lane_base, iv);  // 1/norm for the epiloguer's Jacobian
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          tc_fence_before();
+          store_split_half(Z, X, s.row, s.h, s.x);
+          if (s.h == 0) inv_st[s.row] = iv;  // 1/norm for the epiloguer's Jacobian
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&br->split_full[st]);
+          TCB_TRACE(2, threadIdx.x == 0);
         } else {  // ---------------- epiloguer ----------------
           if (ps == 0 && c == C - 1) {
             // G complete: dm = -ln(n) s <G, S> (:408), dA = s G (:412-413)
             mbar_wait(&br->red_done, j & 1);
             tc_fence_after();
-            float gr[64];
-            acc_row(tmem, run, wq, lane, C > kFlush, gr);
-            double dot = 0.0;
-            if (lane < 16) {
-              const int a = 16 * wq + lane;
-              dot = (double)dot_state_row(ops, ops + kStateTile, a, gr);
+            float dotf = 0.f;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+              float gr[32];
+              acc_half(tmem, run, wq, lane, h, C > kFlush, gr);
+              if (lane < 16) {
+                const int a = 16 * wq + lane;
+                dotf += dot_state_half(ops, ops + kStateTile, a, h, gr);
 #pragma unroll
-              for (int e = 0; e < 64; ++e) gr[e] *= uc.s;
-              store_state_row(ops + 2 * kStateTile, ops + 3 * kStateTile, a, gr);
+                for (int e = 0; e < 32; ++e) gr[e] *= uc.s;
+                store_split_half(ops + 2 * kStateTile, ops + 3 * kStateTile, a, h, gr);
+              }
             }
+            double dot = (double)dotf;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
             if (lane == 0) dm_x[wq] = dot;
             fence_proxy_async();
             tc_fence_before();
-            tc::group_sync(g);
+            epi_sync();
             if (t == 0) {
               const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
               if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
@@ -751,6 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             }
           }
           mbar_wait(&br->mma_done[st], par3(it));
+          TCB_TRACE(5, t == 0);
           tc_fence_after();
           if (ps == 0 && c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush G
             flush_acc(tmem, run, wq, lane, c == kFlush - 1);
@@ -758,41 +794,62 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             __syncwarp();
             if (lane == 0) mbar_arrive(&br->acc_free);
           }
-          float x[64], gv[64];
-          load_split_row(Z, X, t, x);  // q~ / k~ = hi + lo in fp32 for the Jacobian
-          const float iv = tmem_ld1(tmem + kInv + st + lane_base);
+          const int r = c * kRows + t;
+          const float iv = inv_st[t];
+          const uint32_t Dg = tmem + kBuf0 + kBufCols * st + lane_base + (ps == 0 ? 0u : 64u);
+          // pr = g . x~ over both halves (x~ = hi + lo rebuilt in fp32; g = dQ~ or dK~)
+          float pr = 0.f;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            float g[32], x[32];
+            tmem_ld_half(Dg + 32u * h, g);
+            load_split_half(Z, X, t, h, x);
+            pr += dot32(g, x);
+          }
           if (ps == 0) {
-            // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428)
-            tmem_ld64(D, gv);
+            // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428); staged in Z
+            // (half h reads and then overwrites only its own granules of row t)
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+              float g[32], x[32];
+              tmem_ld_half(Dg + 32u * h, g);
+              load_split_half(Z, X, t, h, x);
 #pragma unroll
-            for (int e = 0; e < 64; ++e) gv[e] *= uc.s;
-            const float pr = dot64(gv, x);
-#pragma unroll
-            for (int e = 0; e < 64; ++e) gv[e] = (gv[e] - pr * x[e]) * iv;
-            store_row(Z, t, gv);
+              for (int e = 0; e < 32; ++e) g[e] = (uc.s * g[e] - uc.s * pr * x[e]) * iv;
+              store_half(Z, t, h, g);
+            }
           } else {
             const bool f = r < N && tc::flag_at(fl, r);
             const bool nan_out = uc.tn == 0;
             // dK_i = v_i ? (g - (g.k~)k~) / nk : 0 (:430-437), staged in Y (V is done)
-            tmem_ld64(D + 64, gv);
-            const float pr = dot64(gv, x);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+              float g[32], x[32];
+              tmem_ld_half(Dg + 32u * h, g);
+              load_split_half(Z, X, t, h, x);
 #pragma unroll
-            for (int e = 0; e < 64; ++e) gv[e] = nan_out ? qnan : (f ? (gv[e] - pr * x[e]) * iv : 0.f);
-            store_row(Y, t, gv);
+              for (int e = 0; e < 32; ++e) g[e] = nan_out ? qnan : (f ? (g[e] - pr * x[e]) * iv : 0.f);
+              store_half(Y, t, h, g);
+            }
             // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439), staged in Z (K~ is done)
-            tmem_ld64(D, gv);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+              float g[32];
+              tmem_ld_half(tmem + kBuf0 + kBufCols * st + lane_base + 32u * h, g);
 #pragma unroll
-            for (int e = 0; e < 64; ++e) gv[e] = nan_out ? qnan : (f ? gv[e] : 0.f);
-            store_row(Z, t, gv);
+              for (int e = 0; e < 32; ++e) g[e] = nan_out ? qnan : (f ? g[e] : 0.f);
+              store_half(Z, t, h, g);
+            }
           }
           arrive_staged(br, st, lane);
+          TCB_TRACE(6, t == 0);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&br->fl_empty[sl]);
     }
   }
-  if (threadIdx.x == 128 && p.dm_total) __threadfence();
+  if (threadIdx.x == 32 * kWarpEpi0 && p.dm_total) __threadfence();
   teardown(tmem, warp);
   if (p.dm_total) tc::last_cta_dm_total(p, units, smem + kOffRing);
 }
@@ -855,6 +912,35 @@ inline cudaError_t launch_tcb_pdl(void (*kern)(KArgs...), int grid, cudaStream_t
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+inline void* tcb_trace_begin(int grid) {
+#if COTTEN_TCB_TRACE
+  static void* buf = nullptr;
+  if (!buf) cudaMalloc(&buf, (size_t)1024 * tcb::kTraceItems * 8 * sizeof(long long));
+  cudaMemset(buf, 0, (size_t)grid * tcb::kTraceItems * 8 * sizeof(long long));
+  return buf;
+#else
+  (void)grid;
+  return nullptr;
+#endif
+}
+inline void tcb_trace_end(void* buf, int grid, const char* tag, cudaStream_t st) {
+#if COTTEN_TCB_TRACE
+  const char* dir = getenv("COTTEN_TRACE_DIR");
+  if (!dir || !buf) return;
+  const size_t n = (size_t)grid * tcb::kTraceItems * 8;
+  std::vector<long long> h(n);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h.data(), buf, n * sizeof(long long), cudaMemcpyDeviceToHost);
+  std::string path = std::string(dir) + "/" + tag + ".bin";
+  if (FILE* f = fopen(path.c_str(), "wb")) {
+    fwrite(h.data(), sizeof(long long), n, f);
+    fclose(f);
+  }
+#else
+  (void)buf; (void)grid; (void)tag; (void)st;
+#endif
+}
+
 inline int launch_tcb_fwd(const OpParams& p, cudaStream_t st) {
   CUtensorMap mq, mk, mv, mo;
   if (!make_bf16_chunk_map(&mq, p.q, p) || !make_bf16_chunk_map(&mk, p.k, p) ||
@@ -864,7 +950,11 @@ inline int launch_tcb_fwd(const OpParams& p, cudaStream_t st) {
                            (int)tcb::kSmemBytes) != cudaSuccess)
     return -1;
   const int grid = std::min((int)(p.B * p.H), sm_count());
-  if (launch_tcb_pdl(tcb::cos_fwd_tcb_kernel, grid, st, mq, mk, mv, mo, p) != cudaSuccess) return -1;
+  OpParams q = p;
+  q.l2_ahead = l2_ahead_items();
+  q.workspace = tcb_trace_begin(grid);
+  if (launch_tcb_pdl(tcb::cos_fwd_tcb_kernel, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
+  tcb_trace_end(q.workspace, grid, "tcb_fwd", st);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 inline int launch_tcb_bwd(const OpParams& p, cudaStream_t st) {
@@ -878,9 +968,13 @@ inline int launch_tcb_bwd(const OpParams& p, cudaStream_t st) {
                            (int)tcb::kSmemBytes) != cudaSuccess)
     return -1;
   const int grid = std::min((int)(p.B * p.H), sm_count());
-  if (launch_tcb_pdl(tcb::cos_bwd_tcb_kernel, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, p) !=
+  OpParams q = p;
+  q.l2_ahead = l2_ahead_items();
+  q.workspace = tcb_trace_begin(grid);
+  if (launch_tcb_pdl(tcb::cos_bwd_tcb_kernel, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, q) !=
       cudaSuccess)
     return -1;
+  tcb_trace_end(q.workspace, grid, "tcb_bwd", st);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
