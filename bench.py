@@ -66,6 +66,17 @@ WORKLOADS = {
 for _name in ("long4k", "long4k_d64", "long4k_d128"):
     _w = WORKLOADS[_name]
     WORKLOADS[_name + "_bf16"] = _w[:6] + (_w[6].replace("fp32", "bf16 in HBM (fp32 arithmetic)"),)
+# BASELINE config #5 sweep grid (scripts/sweep_long.sh): N = 512 ... 16384 x d_h 32 / 64 / 128
+# x fp32 / bf16, 4 M rows of work per tensor per launch (B*H = 4M / N; H = 2 at d_h 32)
+for _n in (512, 1024, 2048, 4096, 8192, 16384):
+    for _d in (32, 64, 128):
+        _h = 2 if _d == 32 else 1
+        for _dt in ("f32", "bf16"):
+            WORKLOADS[f"sw_n{_n}_d{_d}_{_dt}"] = (
+                (1 << 22) // (_n * _h), _n, _h, _d, 1, True,
+                f"BASELINE config #5 sweep point: cosine-attn fwd+bwd, N={_n}, H={_h}, d_h={_d}, "
+                f"B={(1 << 22) // (_n * _h)}, {'fp32' if _dt == 'f32' else 'bf16 in HBM (fp32 arithmetic)'}, "
+                f"left-padded mask")
 WORKLOAD_DTYPE = {n: "bf16" for n in WORKLOADS if n.endswith("_bf16")}
 L2_FLUSH_BYTES = 256 << 20
 
@@ -126,6 +137,19 @@ def kernel_path(path, N, D, dname="f32"):
     if D in (64, 128):
         return "fp32-rt register-tiled FP32 pipe (kernels_rt.cuh)"
     return "generic (kernels_generic.cuh)"
+
+
+def load_tensor_peak():
+    """Dense bf16 tensor FLOP/s: MEASURED_PEAKS.json, else B200_PROFILING.md's 2.25 PF."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        for k in ("bf16_tflops", "dense_bf16_tflops", "cublas_bf16_tflops"):
+            if k in d:
+                return float(d[k]) * 1e12
+    except Exception:
+        pass
+    return 2.25e15
 
 
 def load_peaks():
@@ -439,13 +463,17 @@ def run_ours(args, world, rank, local, with_cpu=True):
                           "step_GBps": step_gbs, "step_frac": step_gbs / peak}
         if D != 32 or dname == "bf16":  # north star: max(compute-at-peak, bytes-at-HBM)
             ff, fb = pipe_flops(B, H, N, D)
-            t_f = max(ff / FP32_PEAK_FLOPS, fwd_bytes / (peak * 1e9))
-            t_b = max(fb / FP32_PEAK_FLOPS, bwd_bytes / (peak * 1e9))
+            kp = kernel_path(args.path, N, D, dname)
+            tensor = kp.startswith("tcgen05")
+            # tensor pipe: the bf16x3 MMAs (3 products) at the measured dense bf16 peak
+            cpeak = (load_tensor_peak() / 3.0) if tensor else FP32_PEAK_FLOPS
+            t_f = max(ff / cpeak, fwd_bytes / (peak * 1e9))
+            t_b = max(fb / cpeak, bwd_bytes / (peak * 1e9))
             res["roofline_max"] = {
-                "model": "max(compute-at-peak, bytes-at-HBM) per launch; compute = the FP32 pipe "
-                         "(148 SM x 128 FFMA x 2 x 1.965 GHz, derived); a kernel on the tensor "
-                         "pipe is bounded by HBM alone",
-                "pipe": "fp32", "peak_tflops": FP32_PEAK_FLOPS / 1e12,
+                "model": "max(compute-at-peak, bytes-at-HBM) per launch; compute = the pipe the "
+                         "kernel runs on: FP32 (148 SM x 128 FFMA x 2 x 1.965 GHz, derived) or the "
+                         "tensor pipe (measured dense bf16 peak / 3 for the bf16x3 products)",
+                "pipe": "tensor" if tensor else "fp32", "peak_tflops": cpeak / 1e12,
                 "fwd_tflops": ff / fwd_avg / 1e12, "bwd_tflops": fb / bwd_avg / 1e12,
                 "fwd_frac": t_f / fwd_avg, "bwd_frac": t_b / bwd_avg,
                 "step_frac": layers * (t_f + t_b) / (ms_per_step / 1e3)}
