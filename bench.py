@@ -126,8 +126,11 @@ def pipe_flops(B, H, N, D):
 
 def kernel_path(path, N, D, dname="f32"):
     """The kernels the library picks for this shape (cotten_capi.cu launch_*_t)."""
-    if dname == "bf16" and D == 64 and path == "tcgen05" and not os.environ.get("COTTEN_NO_TCB"):
+    tcb = path == "tcgen05" and not os.environ.get("COTTEN_NO_TCB")
+    if dname == "bf16" and D == 64 and tcb:
         return "tcgen05 kind::f16 bf16x3 (kernels_tcb.cuh)"
+    if dname == "bf16" and D == 32 and tcb and N % 2 == 0 and not os.environ.get("COTTEN_NO_TCB_PAIR"):
+        return "tcgen05 kind::f16 bf16x3, paired rows (kernels_tcb.cuh)"
     if dname == "bf16" and D == 32:
         return "fp32-rt register-tiled FP32 pipe (kernels_rt.cuh)"
     if D == 32 and path == "tcgen05" and N > 64:

@@ -31,6 +31,17 @@
 // MN-major B of O = Q~ S / dV = K~ dA and the K-major B of dQ~ = dO S^T /
 // dK~ = V dA^T alike.
 //
+// Paired rows (kPair, head_dim 32): a contiguous [N][32] bf16 unit (N even)
+// is read as [N/2][64] — packed row p = rows 2p | 2p+1, one 128-B row — so
+// the same 128-B tiles, TMA boxes and MMAs serve d_h = 32 (attention.cpp has
+// no head-dim restriction).  Each half of a packed row is normalised, masked
+// and differentiated as its own row; the 64 x 64 reduction R' = X'^T Y' holds
+// R = R'00 + R'11 on its diagonal blocks (the off-diagonal blocks pair row 2p
+// with 2p+1 and are discarded), and the state operand is blockdiag(S, S) /
+// blockdiag(dA, dA), so every row output [x_2p | x_2p+1] B' = [x_2p S | x_2p+1 S].
+// The tensor pipe does twice the useful work, which it has to spare; the
+// alternative (64-B rows) would halve every TMA box and MMA K-step.
+//
 // Warp roles (512 threads): 0-7 splitter (two threads per chunk row, 32
 // columns each: a single splitter warp per SMSP was the latency-bound stage,
 // measured), 8-11 epiloguer (thread t = TMEM lane t, rows processed in two
@@ -81,8 +92,9 @@ constexpr uint32_t kStateTile = 64 * 128;  // 64 x 64 bf16 rows
 constexpr uint32_t kOffOps = kOffRing + kRing * kSlot;   // S hi, S lo, dA hi, dA lo
 constexpr uint32_t kOffRun = kOffOps + 4 * kStateTile;   // fp32 running sum, 64 x 64
 constexpr uint32_t kOffFlags = kOffRun + 64 * 64 * 4;    // 2 x 2 KB bitmasks
-constexpr uint32_t kOffInv = kOffFlags + 2 * (kMaxN / 8);  // per slot 128 x 1/norm (bwd)
-constexpr uint32_t kOffMisc = kOffInv + kRing * kRows * 4;
+constexpr uint32_t kOffInv = kOffFlags + 2 * (kMaxN / 8);  // per slot 256 x 1/norm (bwd)
+constexpr uint32_t kOffScr = kOffInv + kRing * 2 * kRows * 4;  // paired rows: 32 x 32 fp32 hand-off
+constexpr uint32_t kOffMisc = kOffScr + 32 * 32 * 4;
 constexpr uint32_t kOffBar = kOffMisc + 128;
 constexpr uint32_t kSmemBytes = kOffBar + 32 * 8;
 static_assert(kSmemBytes <= 227 * 1024, "shared-memory budget");
@@ -370,25 +382,68 @@ struct SplitRow {
   float x[32];
   float ss;  // |row|^2 (both halves)
 };
+// (kPair: each half is a row of its own, so no partner sum.)
+template <bool kPair>
 __device__ __forceinline__ void split_load(const uint8_t* X, int t, SplitRow& s) {
   s.row = t >> 1;
   s.h = t & 1;
   load_half(X, s.row, s.h, s.x);
   const float part = sumsq32(s.x);
-  s.ss = part + __shfl_xor_sync(0xffffffffu, part, 1);
+  s.ss = kPair ? part : part + __shfl_xor_sync(0xffffffffu, part, 1);
+}
+
+// ---- paired rows (d_h = 32) --------------------------------------------------------
+// R = R'00 + R'11 of the finished 64 x 64 accumulator (+ running sum): warps
+// 2-3 (rows 32-63, columns 32-63) hand their rows to warps 0-1 through `scr`
+// (row stride 128 B, float4 k of row a at slot k ^ (a & 7): 2 wavefronts per
+// 16-lane access); on return lanes < 16 of warps 0-1 hold R row 16 wq + lane.
+__device__ __forceinline__ void pair_combine(uint32_t tmem, const float* run, float* scr, int wq,
+                                             int lane, bool with_run, float (&r)[32]) {
+  acc_half(tmem, run, wq, lane, wq >= 2 ? 1 : 0, with_run, r);
+  const int a = 16 * (wq & 1) + lane;
+  if (wq >= 2 && lane < 16) {
+    float4* d = reinterpret_cast<float4*>(scr + a * 32);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      d[k ^ (a & 7)] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+  }
+  epi_sync();
+  if (wq < 2 && lane < 16) {
+    const float4* d = reinterpret_cast<const float4*>(scr + a * 32);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = d[k ^ (a & 7)];
+      r[4 * k] += v.x;
+      r[4 * k + 1] += v.y;
+      r[4 * k + 2] += v.z;
+      r[4 * k + 3] += v.w;
+    }
+  }
+}
+// Row a (< 32) of a 32 x 32 state as rows a and a + 32 of blockdiag(X, X) (bf16 hi / lo).
+__device__ __forceinline__ void store_blockdiag(uint8_t* hi, uint8_t* lo, int a, const float (&x)[32]) {
+  float z[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) z[e] = 0.f;
+  store_split_half(hi, lo, a, 0, x);
+  store_split_half(hi, lo, a, 1, z);
+  store_split_half(hi, lo, a + 32, 0, z);
+  store_split_half(hi, lo, a + 32, 1, x);
 }
 
 // ======================================================================================
 // Forward
 // ======================================================================================
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
     const OpParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = (int)p.N, H = (int)p.H;
+  const int NP = kPair ? (N + 1) >> 1 : N;  // tile rows (packed rows when kPair)
   const int units = (int)(p.B * p.H);
-  const int C = (N + kRows - 1) / kRows;
+  const int C = (NP + kRows - 1) / kRows;
   const int P = (p.out != nullptr || p.saved_norms != nullptr) ? 2 : 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
@@ -450,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
           const uint32_t X = base + kOffRing + st * kSlot, Z = X + 2 * kTile;
           if (elect_one()) {
             if (ps == 0) {  // S += K~^T V (attention.cpp:345-353), K~ = hi (Z) + lo (X)
-              const int ks = (min(kRows, N - c * kRows) + 15) >> 4;
+              const int ks = (min(kRows, NP - c * kRows) + 15) >> 4;
               issue_reduction(tmem, Z, X + kTile, ks, c % kFlush == 0);
               issue_reduction(tmem, X, X + kTile, ks, false);
             } else {  // O = Q~ S (:379-387)
@@ -508,16 +563,18 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
           mbar_wait(&br->raw_full[st], par3(it));
           TCB_TRACE(1, threadIdx.x == 0);
           SplitRow s;
-          split_load(X, t, s);
-          const int r = c * kRows + s.row;
+          split_load<kPair>(X, t, s);
+          // sequence row of this half (kPair: packed row s.row holds rows 2 s.row, 2 s.row + 1)
+          const int r = kPair ? 2 * c * kRows + t : c * kRows + s.row;
+          const bool wr = norms && r < N && (kPair || s.h == 0);
           const float iv = rsqrtf(s.ss + eps);
           if (ps == 0) {  // k~ masked (attention.cpp:334-343)
             const bool f = r < N && tc::flag_at(fl, r);
-            if (norms && r < N && s.h == 0) norms[N + r] = f ? (s.ss + eps) * iv : 1.0f;
+            if (wr) norms[N + r] = f ? (s.ss + eps) * iv : 1.0f;
 #pragma unroll
             for (int e = 0; e < 32; ++e) s.x[e] = f ? s.x[e] * iv : 0.f;  // NaN-safe zeros
           } else {  // q~ every row (:366-377)
-            if (norms && r < N && s.h == 0) norms[r] = (s.ss + eps) * iv;
+            if (wr) norms[r] = (s.ss + eps) * iv;
 #pragma unroll
             for (int e = 0; e < 32; ++e) s.x[e] *= iv;
           }
@@ -537,7 +594,24 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
               __syncwarp();
               if (lane == 0) mbar_arrive(&br->acc_free);
             }
-            if (c == C - 1) {  // S complete: saved S + the bf16 hi / lo state operand
+            if (kPair && c == C - 1) {  // S = S'00 + S'11; operand blockdiag(S, S)
+              float sv[32];
+              pair_combine(tmem, run, reinterpret_cast<float*>(smem + kOffScr), wq, lane, C > kFlush, sv);
+              if (wq < 2 && lane < 16) {
+                const int a = 16 * wq + lane;
+                if (gS_all) {
+                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024 + a * 32);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e)
+                    gs[e] = make_float4(sv[4 * e], sv[4 * e + 1], sv[4 * e + 2], sv[4 * e + 3]);
+                }
+                store_blockdiag(ops, ops + kStateTile, a, sv);
+              }
+              fence_proxy_async();
+              tc_fence_before();
+              epi_sync();
+              if (t == 0) mbar_arrive(&br->op_ready);
+            } else if (c == C - 1) {  // S complete: saved S + the bf16 hi / lo state operand
 #pragma unroll 1
               for (int h = 0; h < 2; ++h) {
                 float sv[32];
@@ -582,6 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
 // ======================================================================================
 // Backward
 // ======================================================================================
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
@@ -589,8 +664,9 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
     const __grid_constant__ CUtensorMap tdv, const OpParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = (int)p.N, H = (int)p.H;
+  const int NP = kPair ? (N + 1) >> 1 : N;  // tile rows (packed rows when kPair)
   const int units = (int)(p.B * p.H);
-  const int C = (N + kRows - 1) / kRows;
+  const int C = (NP + kRows - 1) / kRows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
   UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
@@ -646,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
           if (elect_one()) {
             if (ps == 0) {
               // G += Q~^T dO (attention.cpp:405), Q~ = hi (Z) + lo (X)
-              const int ks = (min(kRows, N - c * kRows) + 15) >> 4;
+              const int ks = (min(kRows, NP - c * kRows) + 15) >> 4;
               issue_reduction(tmem, Z, Y, ks, c % kFlush == 0);
               issue_reduction(tmem, X, Y, ks, false);
               // dQ~ (unscaled) = dO S^T (:410-411): A = dO (K-major), B row n = S row n
@@ -709,17 +785,22 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
         uint8_t* X = smem + kOffRing + st * kSlot;
         uint8_t* Y = X + kTile;
         uint8_t* Z = X + 2 * kTile;
-        float* inv_st = invs + st * kRows;
+        float* inv_st = invs + st * 2 * kRows;
         if (splitter) {  // ---------------- splitter (2 threads per row) ----------------
           if (ps == 0 && c == 0) {
             // this unit's S (saved by the forward) as bf16 hi / lo rows; the previous
             // unit's dQ~ MMAs and G-epilogue (dm) have read its S (op_ready)
             if (j > 0) mbar_wait(&br->op_ready, (j - 1) & 1);
             const int a = t >> 2, q4 = t & 3;  // row a, granules 2 q4, 2 q4 + 1
-            const float4* gs = reinterpret_cast<const float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 16 * q4);
+            // kPair: blockdiag(S, S) — granules 0-3 of rows 0-31 and 4-7 of rows 32-63 hold S
+            const bool live = !kPair || (q4 >> 1) == (a >> 5);
+            const float4* gs = reinterpret_cast<const float4*>(
+                kPair ? gS_all + (int64_t)u * 1024 + (a & 31) * 32 + 16 * (q4 & 1)
+                      : gS_all + (int64_t)u * 4096 + a * 64 + 16 * q4);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-              const float4 v0 = __ldg(gs + 2 * q), v1 = __ldg(gs + 2 * q + 1);
+              const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              const float4 v0 = live ? __ldg(gs + 2 * q) : z4, v1 = live ? __ldg(gs + 2 * q + 1) : z4;
               const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
               float hi[8], lo[8];
 #pragma unroll
@@ -736,8 +817,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
           mbar_wait(&br->raw_full[st], par3(it));
           TCB_TRACE(1, threadIdx.x == 0);
           SplitRow s;
-          split_load(X, t, s);
-          const int r = c * kRows + s.row;
+          split_load<kPair>(X, t, s);
+          const int r = kPair ? 2 * c * kRows + t : c * kRows + s.row;
           const float iv = rsqrtf(s.ss + eps);
           if (ps == 0) {  // q~ (rows past N: exact zeros in G even for eps = 0)
             const float sc = r < N ? iv : 0.f;
@@ -749,7 +830,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             for (int e = 0; e < 32; ++e) s.x[e] = f ? s.x[e] * iv : 0.f;
           }
           store_split_half(Z, X, s.row, s.h, s.x);
-          if (s.h == 0) inv_st[s.row] = iv;  // 1/norm for the epiloguer's Jacobian
+          if (kPair)
+            inv_st[t] = iv;  // 1/norm of row 2 s.row + s.h for the epiloguer's Jacobian
+          else if (s.h == 0)
+            inv_st[s.row] = iv;
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&br->split_full[st]);
@@ -760,16 +844,28 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             mbar_wait(&br->red_done, j & 1);
             tc_fence_after();
             float dotf = 0.f;
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
+            if (kPair) {  // G = G'00 + G'11; dA operand blockdiag(s G, s G)
               float gr[32];
-              acc_half(tmem, run, wq, lane, h, C > kFlush, gr);
-              if (lane < 16) {
+              pair_combine(tmem, run, reinterpret_cast<float*>(smem + kOffScr), wq, lane, C > kFlush, gr);
+              if (wq < 2 && lane < 16) {
                 const int a = 16 * wq + lane;
-                dotf += dot_state_half(ops, ops + kStateTile, a, h, gr);
+                dotf = dot_state_half(ops, ops + kStateTile, a, 0, gr);  // S row a = op row a, half 0
 #pragma unroll
                 for (int e = 0; e < 32; ++e) gr[e] *= uc.s;
-                store_split_half(ops + 2 * kStateTile, ops + 3 * kStateTile, a, h, gr);
+                store_blockdiag(ops + 2 * kStateTile, ops + 3 * kStateTile, a, gr);
+              }
+            } else {
+#pragma unroll 1
+              for (int h = 0; h < 2; ++h) {
+                float gr[32];
+                acc_half(tmem, run, wq, lane, h, C > kFlush, gr);
+                if (lane < 16) {
+                  const int a = 16 * wq + lane;
+                  dotf += dot_state_half(ops, ops + kStateTile, a, h, gr);
+#pragma unroll
+                  for (int e = 0; e < 32; ++e) gr[e] *= uc.s;
+                  store_split_half(ops + 2 * kStateTile, ops + 3 * kStateTile, a, h, gr);
+                }
               }
             }
             double dot = (double)dotf;
@@ -794,18 +890,22 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             __syncwarp();
             if (lane == 0) mbar_arrive(&br->acc_free);
           }
-          const int r = c * kRows + t;
-          const float iv = inv_st[t];
+          // per half h: its sequence row, 1/norm and g . x~ (kPair: each half is a row;
+          // otherwise both halves are one row)
+          const int r0 = kPair ? 2 * (c * kRows + t) : c * kRows + t;
+          const float iv0 = kPair ? inv_st[2 * t] : inv_st[t];
+          const float iv1 = kPair ? inv_st[2 * t + 1] : iv0;
           const uint32_t Dg = tmem + kBuf0 + kBufCols * st + lane_base + (ps == 0 ? 0u : 64u);
-          // pr = g . x~ over both halves (x~ = hi + lo rebuilt in fp32; g = dQ~ or dK~)
-          float pr = 0.f;
+          // pr = g . x~ (x~ = hi + lo rebuilt in fp32; g = dQ~ or dK~)
+          float pr0 = 0.f, pr1 = 0.f;
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
             float g[32], x[32];
             tmem_ld_half(Dg + 32u * h, g);
             load_split_half(Z, X, t, h, x);
-            pr += dot32(g, x);
+            (h == 0 ? pr0 : pr1) = dot32(g, x);
           }
+          if (!kPair) pr1 = pr0 = pr0 + pr1;
           if (ps == 0) {
             // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428); staged in Z
             // (half h reads and then overwrites only its own granules of row t)
@@ -814,12 +914,14 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
               float g[32], x[32];
               tmem_ld_half(Dg + 32u * h, g);
               load_split_half(Z, X, t, h, x);
+              const float pr = h ? pr1 : pr0, iv = h ? iv1 : iv0;
 #pragma unroll
               for (int e = 0; e < 32; ++e) g[e] = (uc.s * g[e] - uc.s * pr * x[e]) * iv;
               store_half(Z, t, h, g);
             }
           } else {
-            const bool f = r < N && tc::flag_at(fl, r);
+            const bool f0 = r0 < N && tc::flag_at(fl, r0);
+            const bool f1 = kPair ? (r0 + 1 < N && tc::flag_at(fl, r0 + 1)) : f0;
             const bool nan_out = uc.tn == 0;
             // dK_i = v_i ? (g - (g.k~)k~) / nk : 0 (:430-437), staged in Y (V is done)
 #pragma unroll 1
@@ -827,6 +929,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
               float g[32], x[32];
               tmem_ld_half(Dg + 32u * h, g);
               load_split_half(Z, X, t, h, x);
+              const float pr = h ? pr1 : pr0, iv = h ? iv1 : iv0;
+              const bool f = h ? f1 : f0;
 #pragma unroll
               for (int e = 0; e < 32; ++e) g[e] = nan_out ? qnan : (f ? (g[e] - pr * x[e]) * iv : 0.f);
               store_half(Y, t, h, g);
@@ -836,6 +940,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             for (int h = 0; h < 2; ++h) {
               float g[32];
               tmem_ld_half(tmem + kBuf0 + kBufCols * st + lane_base + 32u * h, g);
+              const bool f = h ? f1 : f0;
 #pragma unroll
               for (int e = 0; e < 32; ++e) g[e] = nan_out ? qnan : (f ? g[e] : 0.f);
               store_half(Z, t, h, g);
@@ -858,12 +963,16 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
 
 // ---- host side ----------------------------------------------------------------------
 
-// 4-D bf16 map over (D, N, H, B), box (64, 128, 1, 1), 128-byte swizzle.
+// 4-D bf16 map over (D, N, H, B), box (64, 128, 1, 1), 128-byte swizzle; for
+// paired rows (d_h = 32, contiguous rows, N even) over (64, N / 2, H, B).
+inline bool tcb_pair(const OpParams& p) { return p.D == 32; }
 inline bool make_bf16_chunk_map(CUtensorMap* map, const void* base, const OpParams& p) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)p.N, (cuuint64_t)p.H, (cuuint64_t)p.B};
-  cuuint64_t strides[3] = {(cuuint64_t)p.sn * 2, (cuuint64_t)p.sh * 2, (cuuint64_t)p.sb * 2};
+  const bool pair = tcb_pair(p);
+  cuuint64_t dims[4] = {64, (cuuint64_t)(pair ? p.N / 2 : p.N), (cuuint64_t)p.H, (cuuint64_t)p.B};
+  cuuint64_t strides[3] = {(cuuint64_t)p.sn * 2 * (pair ? 2 : 1), (cuuint64_t)p.sh * 2,
+                           (cuuint64_t)p.sb * 2};
   cuuint32_t box[4] = {64, (cuuint32_t)tcb::kRows, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
@@ -872,7 +981,12 @@ inline bool make_bf16_chunk_map(CUtensorMap* map, const void* base, const OpPara
 }
 
 inline bool tcb_layout_ok(const OpParams& p, std::initializer_list<const void*> ptrs) {
-  if (p.D != 64 || p.N < 1 || p.N > tcb::kMaxN) return false;
+  if (p.N < 1 || p.N > tcb::kMaxN) return false;
+  if (p.D == 32) {  // paired rows: [N][32] read as [N/2][64]
+    if (p.sn != 32 || (p.N & 1) || getenv("COTTEN_NO_TCB_PAIR")) return false;
+  } else if (p.D != 64) {
+    return false;
+  }
   if ((p.sn * 2) % 16 || (p.sh * 2) % 16 || (p.sb * 2) % 16) return false;
   if (p.B * p.H > (1ll << 31) - 1) return false;
   for (const void* q : ptrs)
@@ -946,14 +1060,15 @@ inline int launch_tcb_fwd(const OpParams& p, cudaStream_t st) {
   if (!make_bf16_chunk_map(&mq, p.q, p) || !make_bf16_chunk_map(&mk, p.k, p) ||
       !make_bf16_chunk_map(&mv, p.v, p) || !make_bf16_chunk_map(&mo, p.out ? p.out : p.q, p))
     return -1;
-  if (cudaFuncSetAttribute(tcb::cos_fwd_tcb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = tcb_pair(p) ? tcb::cos_fwd_tcb_kernel<true> : tcb::cos_fwd_tcb_kernel<false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tcb::kSmemBytes) != cudaSuccess)
     return -1;
   const int grid = std::min((int)(p.B * p.H), sm_count());
   OpParams q = p;
   q.l2_ahead = l2_ahead_items();
   q.workspace = tcb_trace_begin(grid);
-  if (launch_tcb_pdl(tcb::cos_fwd_tcb_kernel, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
+  if (launch_tcb_pdl(kern, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
   tcb_trace_end(q.workspace, grid, "tcb_fwd", st);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
@@ -964,15 +1079,15 @@ inline int launch_tcb_bwd(const OpParams& p, cudaStream_t st) {
       !make_bf16_chunk_map(&mdq, p.dq, p) || !make_bf16_chunk_map(&mdk, p.dk, p) ||
       !make_bf16_chunk_map(&mdv, p.dv, p))
     return -1;
-  if (cudaFuncSetAttribute(tcb::cos_bwd_tcb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = tcb_pair(p) ? tcb::cos_bwd_tcb_kernel<true> : tcb::cos_bwd_tcb_kernel<false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tcb::kSmemBytes) != cudaSuccess)
     return -1;
   const int grid = std::min((int)(p.B * p.H), sm_count());
   OpParams q = p;
   q.l2_ahead = l2_ahead_items();
   q.workspace = tcb_trace_begin(grid);
-  if (launch_tcb_pdl(tcb::cos_bwd_tcb_kernel, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, q) !=
-      cudaSuccess)
+  if (launch_tcb_pdl(kern, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, q) != cudaSuccess)
     return -1;
   tcb_trace_end(q.workspace, grid, "tcb_bwd", st);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
