@@ -17,7 +17,7 @@ for f in sorted(glob.glob(os.path.join(sys.argv[1], "sw_*.json"))):
                  k.get("fwd_frac"), k.get("bwd_frac"), k.get("step_frac"), rm.get("step_frac"),
                  d["run"]["kernel_path"], d["clocks"]["sm_mhz"], ",".join(d["clocks"]["reasons"])))
 rows.sort()
-print("| N | d_h | dtype | B | seq/s | fwd frac | bwd frac | step frac (HBM) | step frac of max(FP32, HBM) | kernels | SM MHz | throttle |")
+print("| N | d_h | dtype | B | seq/s | fwd frac | bwd frac | step frac (HBM) | step frac of max(compute, HBM) (compute = the pipe used) | kernels | SM MHz | throttle |")
 print("|---|---|---|---|---|---|---|---|---|---|---|---|")
 f = lambda x: "-" if x is None else f"{x:.3f}"  # noqa: E731
 for r in rows:
