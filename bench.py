@@ -133,6 +133,8 @@ def kernel_path(path, N, D, dname="f32"):
         return "tcgen05 kind::f16 bf16x3, paired rows (kernels_tcb.cuh)"
     if dname == "bf16" and D == 32:
         return "fp32-rt register-tiled FP32 pipe (kernels_rt.cuh)"
+    if dname == "f32" and D == 64 and tcb and not os.environ.get("COTTEN_NO_TCF"):
+        return "tcgen05 kind::f16, fp32 as three bf16 parts (kernels_tcf.cuh)"
     if D == 32 and path == "tcgen05" and N > 64:
         return "tcgen05 (kernels_tc.cuh)"
     if D == 32:
@@ -468,14 +470,17 @@ def run_ours(args, world, rank, local, with_cpu=True):
             ff, fb = pipe_flops(B, H, N, D)
             kp = kernel_path(args.path, N, D, dname)
             tensor = kp.startswith("tcgen05")
-            # tensor pipe: the bf16x3 MMAs (3 products) at the measured dense bf16 peak
-            cpeak = (load_tensor_peak() / 3.0) if tensor else FP32_PEAK_FLOPS
+            # tensor pipe at the measured dense bf16 peak / the products per useful
+            # product: 3 (bf16x3, bf16 inputs) or 6 (fp32 as three bf16 parts)
+            nprod = 6 if "three bf16 parts" in kp else 3
+            cpeak = (load_tensor_peak() / nprod) if tensor else FP32_PEAK_FLOPS
             t_f = max(ff / cpeak, fwd_bytes / (peak * 1e9))
             t_b = max(fb / cpeak, bwd_bytes / (peak * 1e9))
             res["roofline_max"] = {
                 "model": "max(compute-at-peak, bytes-at-HBM) per launch; compute = the pipe the "
                          "kernel runs on: FP32 (148 SM x 128 FFMA x 2 x 1.965 GHz, derived) or the "
-                         "tensor pipe (measured dense bf16 peak / 3 for the bf16x3 products)",
+                         "tensor pipe (measured dense bf16 peak / 3 for the bf16x3 products, / 6 for fp32 "
+                         "as three bf16 parts)",
                 "pipe": "tensor" if tensor else "fp32", "peak_tflops": cpeak / 1e12,
                 "fwd_tflops": ff / fwd_avg / 1e12, "bwd_tflops": fb / bwd_avg / 1e12,
                 "fwd_frac": t_f / fwd_avg, "bwd_frac": t_b / bwd_avg,

@@ -21,6 +21,7 @@
 #include "kernels_rt.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_tcb.cuh"
+#include "kernels_tcf.cuh"
 
 namespace cotten {
 namespace {
@@ -223,7 +224,12 @@ template <typename T>
 void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
-  if (tensor && tcb_fwd_supported<T>(p)) {
+  if (tensor && tcf_fwd_supported<T>(p)) {
+    const int n = launch_tcf_fwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fp32 d_h=64 tensor-core forward launch failed"};
+    g_launches += n;
+  } else if (tensor && tcb_fwd_supported<T>(p)) {
     const int n = launch_tcb_fwd(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: bf16 tensor-core forward launch failed"};
@@ -256,7 +262,12 @@ template <typename T>
 void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
-  if (tensor && tcb_bwd_supported<T>(p)) {
+  if (tensor && tcf_bwd_supported<T>(p)) {
+    const int n = launch_tcf_bwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fp32 d_h=64 tensor-core backward launch failed"};
+    g_launches += n;
+  } else if (tensor && tcb_bwd_supported<T>(p)) {
     const int n = launch_tcb_bwd(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: bf16 tensor-core backward launch failed"};
@@ -356,7 +367,8 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
   if (dm_total && !dm_unit)
     p.dm_unit = static_cast<double*>(scratch_get(st, kScrDm, L.units() * sizeof(double)));
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
-  const bool tc_path = tensor && ((L.dtype == COTTEN_F32 && tc_bwd_supported<float>(p)) ||
+  const bool tc_path = tensor && ((L.dtype == COTTEN_F32 && (tc_bwd_supported<float>(p) ||
+                                                              tcf_bwd_supported<float>(p))) ||
                                   (L.dtype == COTTEN_BF16 && tcb_bwd_supported<__nv_bfloat16>(p)));
   if (dm_total && tc_path) {  // the tcgen05 kernel's last CTA writes the total (no extra launch)
     p.dm_total = dm_total;
