@@ -270,14 +270,21 @@ def test_bnhd_strided_layout_equals_contiguous():
 @pytest.mark.parametrize("D,dtype", [(64, "f32"), (128, "f32"), (32, "bf16"), (64, "bf16")])
 def test_bnhd_strided_layout_register_tiled(D, dtype):
     """The register-tiled kernels read a [B][N][H*D] projection output in
-    place (stride_n = H*D): identical results to the contiguous layout."""
+    place (stride_n = H*D): identical results to the contiguous layout.
+    (COTTEN_FLAG_FP32_PIPE keeps both layouts on them: contiguous bf16 d_h 32
+    would otherwise take the paired-row tensor-core kernel, fp32 d_h 64 the
+    three-part one.)  The default path on the strided layout stays within
+    the bar of the oracle."""
     B, H, N = 4, 2, 150
     h = inputs.make_host(B, H, N, D, seed=40 + D)
     valid = inputs.left_padded_mask(B, N, 40)
-    a = run_gpu(h, valid, 1.0, 1e-6, dtype, layout="bhnd")
-    b = run_gpu(h, valid, 1.0, 1e-6, dtype, layout="bnhd")
+    fl = _lib.FLAG_FP32_PIPE
+    a = run_gpu(h, valid, 1.0, 1e-6, dtype, layout="bhnd", flags=fl)
+    b = run_gpu(h, valid, 1.0, 1e-6, dtype, layout="bnhd", flags=fl)
     for n in ("out", "dq", "dk", "dv"):
         np.testing.assert_array_equal(a[n], b[n])
+    c = run_gpu(h, valid, 1.0, 1e-6, dtype, layout="bnhd")
+    assert_parity(c, oracle_for(c["inputs"], valid, 1.0, 1e-6), valid, dtype)
 
 
 def test_head_dim_64_long_sequence_accuracy():
