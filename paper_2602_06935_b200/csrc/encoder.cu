@@ -22,6 +22,7 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -285,19 +286,29 @@ __global__ void gelu_bwd_kernel(float* __restrict__ da, const float* __restrict_
 // Column sums over rows (bias / gain gradients, colsum_into encoder.cpp:167-172),
 // deterministic: stage 1 writes per-(row-slab) partials in a fixed order,
 // stage 2 adds them in slab order.  With b != nullptr it sums a * b.
-constexpr int kColSlabs = 64;
+constexpr int kColSlabs = 512;  // max row slabs (partials buffer: kColSlabs x C)
 __global__ void colsum_stage1(const float* __restrict__ a, int lda, const float* __restrict__ b,
-                              int ldb, int64_t R, int C, float* __restrict__ part) {
+                              int ldb, int64_t R, int C, int slabs, float* __restrict__ part) {
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   const int w = threadIdx.x >> 5;  // 8 warps
   const int slab = blockIdx.y;
-  const int64_t per = (R + kColSlabs - 1) / kColSlabs;
+  const int64_t per = (R + slabs - 1) / slabs;
   const int64_t r0 = slab * per, r1 = min(R, r0 + per);
-  float acc = 0.f;
-  if (c < C)
-    for (int64_t r = r0 + w; r < r1; r += 8) acc += b ? a[r * lda + c] * b[r * ldb + c] : a[r * lda + c];
+  // four independent accumulators (rows r, r + 8, r + 16, r + 24 of the warp's
+  // stride-8 sequence) keep four loads in flight; fixed order, deterministic
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (c < C) {
+    int64_t r = r0 + w;
+    for (; r + 24 < r1; r += 32)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t rr = r + 8 * u;
+        acc[u] += b ? a[rr * lda + c] * b[rr * ldb + c] : a[rr * lda + c];
+      }
+    for (; r < r1; r += 8) acc[0] += b ? a[r * lda + c] * b[r * ldb + c] : a[r * lda + c];
+  }
   __shared__ float sh[8][32];
-  sh[w][threadIdx.x & 31] = acc;
+  sh[w][threadIdx.x & 31] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   __syncthreads();
   if (w == 0 && c < C) {
     float t = 0.f;
@@ -305,11 +316,11 @@ __global__ void colsum_stage1(const float* __restrict__ a, int lda, const float*
     part[(int64_t)slab * C + c] = t;
   }
 }
-__global__ void colsum_stage2(const float* __restrict__ part, int C, float* __restrict__ out) {
+__global__ void colsum_stage2(const float* __restrict__ part, int C, int slabs, float* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   float t = 0.f;
-  for (int s = 0; s < kColSlabs; ++s) t += part[(int64_t)s * C + c];
+  for (int s = 0; s < slabs; ++s) t += part[(int64_t)s * C + c];
   out[c] = t;
 }
 
@@ -739,9 +750,12 @@ void gemm_rm(cublasHandle_t h, bool ta, bool tb, int64_t M, int64_t N, int64_t K
 
 void colsum(cotten_encoder* e, const float* a, int64_t lda, const float* b, int64_t ldb, int64_t R,
             int64_t C, float* out, cudaStream_t st) {
-  dim3 g1((unsigned)((C + 31) / 32), kColSlabs);
-  colsum_stage1<<<g1, 256, 0, st>>>(a, (int)lda, b, (int)ldb, R, (int)C, e->col_part);
-  colsum_stage2<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(e->col_part, (int)C, out);
+  // ~4 CTAs per SM over (column groups x row slabs), >= 64 rows per slab
+  const int cg = (int)((C + 31) / 32);
+  const int slabs = (int)std::max<int64_t>(1, std::min<int64_t>({kColSlabs, 592 / cg, (R + 63) / 64}));
+  dim3 g1((unsigned)cg, (unsigned)slabs);
+  colsum_stage1<<<g1, 256, 0, st>>>(a, (int)lda, b, (int)ldb, R, (int)C, slabs, e->col_part);
+  colsum_stage2<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(e->col_part, (int)C, slabs, out);
 }
 
 cotten_desc op_desc(const cotten_encoder* e, int64_t B, int64_t n) {

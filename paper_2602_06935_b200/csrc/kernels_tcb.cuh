@@ -169,14 +169,15 @@ __device__ __forceinline__ void store_split_half(uint8_t* hi_tile, uint8_t* lo_t
                                                  const float (&x)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    float hi[8], lo[8];
+    uint32_t hw[4], lw[4];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      hi[e] = __bfloat162float(__float2bfloat16_rn(x[8 * q + e]));
-      lo[e] = x[8 * q + e] - hi[e];
+    for (int e = 0; e < 4; ++e) {  // one cvt.rn.bf16x2.f32 per pair; bf16 -> fp32 is a shift
+      const float x0 = x[8 * q + 2 * e], x1 = x[8 * q + 2 * e + 1];
+      hw[e] = pack2(x0, x1);
+      lw[e] = pack2(x0 - __uint_as_float(hw[e] << 16), x1 - __uint_as_float(hw[e] & 0xFFFF0000u));
     }
-    *reinterpret_cast<uint4*>(hi_tile + goff(row, 4 * h + q)) = pack8(hi);
-    *reinterpret_cast<uint4*>(lo_tile + goff(row, 4 * h + q)) = pack8(lo);
+    *reinterpret_cast<uint4*>(hi_tile + goff(row, 4 * h + q)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(lo_tile + goff(row, 4 * h + q)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
 }
 __device__ __forceinline__ void load_split_half(const uint8_t* hi_tile, const uint8_t* lo_tile,

@@ -112,22 +112,25 @@ struct Bars {
 static_assert(sizeof(Bars) <= 256, "barrier area");
 
 // ---- three-part bf16 split ----------------------------------------------------------
-__device__ __forceinline__ void split3(float x, float& b0, float& b1, float& b2) {
-  b0 = __bfloat162float(__float2bfloat16_rn(x));
-  const float r1 = x - b0;  // exact
-  b1 = __bfloat162float(__float2bfloat16_rn(r1));
-  b2 = __bfloat162float(__float2bfloat16_rn(r1 - b1));
+__device__ __forceinline__ uint32_t bf2_bits(__nv_bfloat162 h) { return *reinterpret_cast<uint32_t*>(&h); }
+// (x0, x1) -> three packed bf16x2 words: one cvt.rn.bf16x2.f32 per part, the
+// unpacking back to fp32 is a shift / mask (bf16 is the top half of an fp32).
+__device__ __forceinline__ void split3_pair(float x0, float x1, uint32_t& w0, uint32_t& w1, uint32_t& w2) {
+  w0 = bf2_bits(__floats2bfloat162_rn(x0, x1));
+  const float r0 = x0 - __uint_as_float(w0 << 16), r1 = x1 - __uint_as_float(w0 & 0xFFFF0000u);  // exact
+  w1 = bf2_bits(__floats2bfloat162_rn(r0, r1));
+  w2 = bf2_bits(__floats2bfloat162_rn(r0 - __uint_as_float(w1 << 16), r1 - __uint_as_float(w1 & 0xFFFF0000u)));
 }
 // 8 values -> parts 0-2 at granule j of row `row` of three part tiles
 __device__ __forceinline__ void store_parts8(uint8_t* p0, uint8_t* p1, uint8_t* p2, int row, int j,
                                              const float* x) {
-  float a[8], b[8], c[8];
+  uint32_t a[4], b[4], c[4];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) split3(x[e], a[e], b[e], c[e]);
+  for (int e = 0; e < 4; ++e) split3_pair(x[2 * e], x[2 * e + 1], a[e], b[e], c[e]);
   const uint32_t o = goff(row, j);
-  *reinterpret_cast<uint4*>(p0 + o) = tcb::pack8(a);
-  *reinterpret_cast<uint4*>(p1 + o) = tcb::pack8(b);
-  *reinterpret_cast<uint4*>(p2 + o) = tcb::pack8(c);
+  *reinterpret_cast<uint4*>(p0 + o) = make_uint4(a[0], a[1], a[2], a[3]);
+  *reinterpret_cast<uint4*>(p1 + o) = make_uint4(b[0], b[1], b[2], b[3]);
+  *reinterpret_cast<uint4*>(p2 + o) = make_uint4(c[0], c[1], c[2], c[3]);
 }
 // parts 0-2 at granule j of row `row` rebuilt in fp32 (b0 + b1 + b2 = x exactly)
 __device__ __forceinline__ void load_parts8(const uint8_t* p0, const uint8_t* p1, const uint8_t* p2,
@@ -298,6 +301,11 @@ __device__ __forceinline__ void store_state_half(uint8_t* ops3, int a, int h, co
 
 // Splitter: four threads per chunk row (16 columns each: fp32 box q / 2,
 // granules 4 (q % 2) .. +3); the row's squared norm is the sum over the quad.
+// Threads q = 2, 3 walk their granules starting at the third: an LDS.128 is
+// served 8 lanes (two rows) per wavefront, and in natural order lanes q and
+// q + 2 of a row would hit the same bank group of the two boxes (2-way
+// conflicts, measured); rotated, the 8 lanes cover all 8 bank groups.  x[]
+// then holds columns 8-15 before 0-7 for q >= 2 (split_store undoes it).
 struct SplitRow {
   int row, q;
   float x[16];
@@ -308,7 +316,7 @@ __device__ __forceinline__ void split_load(const uint8_t* X, int t, SplitRow& s,
   s.q = t & 3;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float4 v = ld_f4(X, s.row, s.q >> 1, 4 * (s.q & 1) + k);
+    const float4 v = ld_f4(X, s.row, s.q >> 1, 4 * (s.q & 1) + ((k + 2 * (s.q >> 1)) & 3));
     s.x[4 * k] = v.x;
     s.x[4 * k + 1] = v.y;
     s.x[4 * k + 2] = v.z;
@@ -330,8 +338,9 @@ __device__ __forceinline__ void split_load(const uint8_t* X, int t, SplitRow& s,
 // part 1 over box 1 (granules 2q, 2q + 1 of the 128-B bf16 row), part 2 into
 // P2.  Call after a __syncwarp that follows every split_load of the warp.
 __device__ __forceinline__ void split_store(uint8_t* X, uint8_t* P2, const SplitRow& s) {
-  store_parts8(X, X + kBox, P2, s.row, 2 * s.q, s.x);
-  store_parts8(X, X + kBox, P2, s.row, 2 * s.q + 1, s.x + 8);
+  const int sw = s.q >> 1;  // rotated load order (split_load)
+  store_parts8(X, X + kBox, P2, s.row, 2 * s.q + sw, s.x);
+  store_parts8(X, X + kBox, P2, s.row, 2 * s.q + 1 - sw, s.x + 8);
 }
 
 // ======================================================================================
