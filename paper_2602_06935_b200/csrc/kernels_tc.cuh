@@ -1018,7 +1018,12 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
             tc_fence_after();
             TC_TRACE(3);
             if (ps == 0) {
+              // a pass-1 item stages nothing and its MMAs are done: release the slot
+              // before the flush / S-epilogue, which work in TMEM and the operand
+              // area only (the splitter may refill the slot meanwhile)
+              arrive_staged(br, bf, lane);
               uint8_t* run = ops + 2 * kOpBytes;  // 8 KB the forward does not otherwise use
+              uint8_t* scr = ops + 4 * kOpBytes;  // and 8 KB more: the S-epilogue's scratch
               if (c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
                 flush_acc(tmem, run, wq, lane, c == kFlush - 1);
                 tc_fence_before();
@@ -1027,7 +1032,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
               }
               if (c == C - 1) {  // S complete: saved S + the MN-major B operand of O = Q~ S
                 float s8[8], h8[8], l8[8];
-                reduce_rows8(tmem, Y + kTile, wq, lane, g, t, s8, C > kFlush ? run : nullptr);
+                reduce_rows8(tmem, scr, wq, lane, g, t, s8, C > kFlush ? run : nullptr);
                 const int a = t >> 2, q = t & 3;
                 if (gS_all) {  // coalesced: a warp writes 8 whole rows of S
                   float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 1024 + a * 32 + 8 * q);
@@ -1048,10 +1053,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
               tc_fence_before();
               scale32(acc, uc.s);
               store_row(Y, t, acc);
+              TC_TRACE(5);
+              arrive_staged(br, bf, lane);
+              TC_TRACE(4);
             }
-            TC_TRACE(5);
-            arrive_staged(br, bf, lane);
-            TC_TRACE(4);
             ++n_tr;
           }
         }
@@ -1499,12 +1504,19 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, cudaStream_t st,
 
 // L2 prefetch distance of the tcgen05 producers (items); COTTEN_L2_AHEAD
 // overrides it (0 = off) for A/B runs.
-inline int l2_ahead_items() {
-  static const int v = [] {
+// L2 prefetch distance (items) of the tcgen05 producers: COTTEN_L2_AHEAD if
+// set, else 4 items for a forward whose units span >= 8 chunks and 0
+// otherwise.  Measured (profiles/r02g_tcb_trace/l2_prefetch_ab.txt): the
+// forward gains at long N (N = 4096 d_h 32: 0.85 -> 0.92; bf16 d_h 64:
+// 0.50 -> 0.54), short units lose (ML-1M 0.42 -> 0.40) and every backward
+// loses (its ring already holds two tensors per item).
+inline int l2_ahead_items(bool forward = false, int chunks = 0) {
+  static const int env = [] {
     const char* e = getenv("COTTEN_L2_AHEAD");
-    return e ? atoi(e) : 0;  // off: measured neutral-to-negative
+    return e ? atoi(e) : -1;
   }();
-  return v;
+  if (env >= 0) return env;
+  return forward && chunks >= 8 ? 4 : 0;
 }
 
 inline int launch_tc_fwd(const OpParams& p, cudaStream_t st) {
@@ -1518,7 +1530,7 @@ inline int launch_tc_fwd(const OpParams& p, cudaStream_t st) {
     return -1;
   const int grid = std::min(units, sm_count());
   OpParams q = p;
-  q.l2_ahead = l2_ahead_items();
+  q.l2_ahead = l2_ahead_items(true, (int)((p.N + tc::kRows - 1) / tc::kRows));
   q.workspace = tc_trace_begin(grid);
   if (launch_pdl(tc::cos_fwd_tc_kernel, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
   tc_trace_end(q.workspace, grid, "fwd", st);

@@ -589,6 +589,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
           TCB_TRACE(5, t == 0);
           tc_fence_after();
           if (ps == 0) {
+            // a pass-1 item stages nothing and its MMAs are done: release the slot
+            // before the flush / S-epilogue (TMEM, the running sum and the operand
+            // area only), so the splitter can refill it meanwhile
+            arrive_staged(br, st, lane);
             if (c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
               flush_acc(tmem, run, wq, lane, c == kFlush - 1);
               tc_fence_before();
@@ -642,8 +646,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
               for (int e = 0; e < 32; ++e) o[e] *= uc.s;
               store_half(Z, t, h, o);
             }
+            arrive_staged(br, st, lane);
           }
-          arrive_staged(br, st, lane);
           TCB_TRACE(6, t == 0);
         }
       }
@@ -1067,7 +1071,7 @@ inline int launch_tcb_fwd(const OpParams& p, cudaStream_t st) {
     return -1;
   const int grid = std::min((int)(p.B * p.H), sm_count());
   OpParams q = p;
-  q.l2_ahead = l2_ahead_items();
+  q.l2_ahead = l2_ahead_items(true, (int)(((tcb_pair(p) ? p.N / 2 : p.N) + tcb::kRows - 1) / tcb::kRows));
   q.workspace = tcb_trace_begin(grid);
   if (launch_tcb_pdl(kern, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
   tcb_trace_end(q.workspace, grid, "tcb_fwd", st);

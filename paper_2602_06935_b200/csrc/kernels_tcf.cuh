@@ -376,6 +376,12 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            tc::ItemPos f;
+            if (p.l2_ahead && tc::item_pos(it + p.l2_ahead, P, C, units, H, f))
+              for (int hb = 0; hb < 2; ++hb) {  // L2 prefetch of a later item (long N)
+                tc::tma_prefetch_4d(f.ps == 0 ? &tk : &tq, 32 * hb, f.c * kRows, f.h, f.b);
+                if (f.ps == 0) tc::tma_prefetch_4d(&tv, 32 * hb, f.c * kRows, f.h, f.b);
+              }
             mbar_wait(&br->slot_free[st], par3(it) ^ 1u);
             uint8_t* X = smem + kOffRing + st * kSlot;
             if (ps == 0) {
@@ -492,6 +498,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
           mbar_wait(&br->mma_done[st], par3(it));
           tc_fence_after();
           if (ps == 0) {
+            // a pass-1 item stages nothing and its MMAs are done: release the slot
+            // before the flush / S-epilogue (TMEM, the running sum and the operand
+            // area only), so the splitter can refill it meanwhile
+            arrive_staged(br, st, lane);
             if (c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
               flush_acc(tmem, run, wq, lane, c == kFlush - 1);
               tc_fence_before();
@@ -527,8 +537,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
             for (int k = 0; k < 8; ++k)
               st_f4(Y, row, h, k, make_float4(o[4 * k] * uc.s, o[4 * k + 1] * uc.s, o[4 * k + 2] * uc.s,
                                               o[4 * k + 3] * uc.s));
+            arrive_staged(br, st, lane);
           }
-          arrive_staged(br, st, lane);
         }
       }
       __syncwarp();
@@ -882,7 +892,9 @@ inline int launch_tcf_fwd(const OpParams& p, cudaStream_t st) {
                            (int)tcf::kSmemBytes) != cudaSuccess)
     return -1;
   const int grid = std::min((int)(p.B * p.H), sm_count());
-  if (launch_tcf_pdl(tcf::cos_fwd_tcf_kernel, grid, st, mq, mk, mv, mo, p) != cudaSuccess) return -1;
+  OpParams q = p;
+  q.l2_ahead = l2_ahead_items(true, (int)((p.N + tcf::kRows - 1) / tcf::kRows));
+  if (launch_tcf_pdl(tcf::cos_fwd_tcf_kernel, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 inline int launch_tcf_bwd(const OpParams& p, cudaStream_t st) {
