@@ -124,7 +124,7 @@ def pipe_flops(B, H, N, D):
     return B * H * (4 * N * D * D + 7 * N * D), B * H * (8 * N * D * D + 12 * N * D)
 
 
-def kernel_path(path, N, D, dname="f32"):
+def kernel_path(path, N, D, dname="f32", H=2):
     """The kernels the library picks for this shape (cotten_capi.cu launch_*_t)."""
     tcb = path == "tcgen05" and not os.environ.get("COTTEN_NO_TCB")
     if dname == "bf16" and D == 64 and tcb:
@@ -137,6 +137,9 @@ def kernel_path(path, N, D, dname="f32"):
         return "tcgen05 kind::f16, fp32 as three bf16 parts (kernels_tcf.cuh)"
     if D == 32 and path == "tcgen05" and N > 64:
         return "tcgen05 (kernels_tc.cuh)"
+    if D == 32 and tcb and H % 2 == 0 and not os.environ.get("COTTEN_NO_TCF") \
+            and not os.environ.get("COTTEN_NO_TCF_MERGE"):
+        return "tcgen05 kind::f16, fp32 as three bf16 parts, head pairs merged (kernels_tcf.cuh)"
     if D == 32:
         return "fp32pipe (kernels_d32.cuh)"
     if D in (64, 128):
@@ -439,7 +442,7 @@ def run_ours(args, world, rank, local, with_cpu=True):
         "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": dname,
         "data": "synthetic U(-1,1) (mix_seed per shape, bench.cpp:21-26,50), left-padded masks",
         "config": workload_config(args.workload, world),
-        "run": {"kernel_path": kernel_path(args.path, N, D, dname),
+        "run": {"kernel_path": kernel_path(args.path, N, D, dname, H),
                 "shard": [lo, hi],
                 "launch": ("eager" if not use_graph else
                            "one CUDA graph per step (programmatic-dependent-launch edges between "
@@ -466,9 +469,10 @@ def run_ours(args, world, rank, local, with_cpu=True):
         res["kernels"] = {"fwd_us": fwd_avg * 1e6, "fwd_GBps": fwd_gbs, "fwd_frac": fwd_gbs / peak,
                           "bwd_us": bwd_avg * 1e6, "bwd_GBps": bwd_gbs, "bwd_frac": bwd_gbs / peak,
                           "step_GBps": step_gbs, "step_frac": step_gbs / peak}
-        if D != 32 or dname == "bf16":  # north star: max(compute-at-peak, bytes-at-HBM)
+        if D != 32 or dname == "bf16" or "three bf16 parts" in kernel_path(args.path, N, D, dname, H):
+            # north star: max(compute-at-peak, bytes-at-HBM)
             ff, fb = pipe_flops(B, H, N, D)
-            kp = kernel_path(args.path, N, D, dname)
+            kp = kernel_path(args.path, N, D, dname, H)
             tensor = kp.startswith("tcgen05")
             # tensor pipe at the measured dense bf16 peak / the products per useful
             # product: 3 (bf16x3, bf16 inputs) or 6 (fp32 as three bf16 parts)

@@ -30,6 +30,15 @@
 // becomes parts 0 | 1 in place, Y likewise, plus X part 2 and Y part 2.
 // Outputs are staged as fp32 boxes over X or Y once the item's MMAs are done.
 //
+// Head-merged mode (kMerge, fp32 d_h = 32, even H, N <= 64 — the Beauty /
+// Steam shape, where a 128-row chunk of the d_h = 32 kernels is 61 % padding):
+// heads 2j and 2j + 1 of one sequence ride in the two 32-column boxes of a
+// 64-column row (box hb is loaded from head 2j + hb), so one 64-row chunk
+// carries both heads' 50 rows.  They share the mask and true_n; each half is
+// normalised and differentiated as its own row; the reduction's diagonal
+// blocks are S_2j and S_2j+1 (the off-diagonal blocks pair the two heads and
+// are discarded), and the state operand is blockdiag(S_2j, S_2j+1).
+//
 // Warp roles (512 threads): 0-7 splitter (four threads per row, 16 columns
 // each; the in-place part writes follow a __syncwarp, since a row's four
 // threads share a warp), 8-11 epiloguer (two threads per row: the M = 64
@@ -88,8 +97,8 @@ constexpr uint32_t kOffRing = 0;
 constexpr uint32_t kOffOps = kOffRing + kRing * kSlot;   // S parts 0-2, dA parts 0-2
 constexpr uint32_t kOffRun = kOffOps + 6 * kBox;         // fp32 running sum, 64 x 64
 constexpr uint32_t kOffFlags = kOffRun + 64 * 64 * 4;    // 2 x 2 KB bitmasks
-constexpr uint32_t kOffInv = kOffFlags + 2 * (kMaxN / 8);  // per slot 64 x 1/norm (bwd)
-constexpr uint32_t kOffMisc = kOffInv + kRing * kRows * 4;
+constexpr uint32_t kOffInv = kOffFlags + 2 * (kMaxN / 8);  // per slot 64 x 2 x 1/norm (bwd)
+constexpr uint32_t kOffMisc = kOffInv + kRing * 2 * kRows * 4;
 constexpr uint32_t kOffBar = kOffMisc + 128;
 constexpr uint32_t kSmemBytes = kOffBar + 32 * 8;
 static_assert(kSmemBytes <= 227 * 1024, "shared-memory budget");
@@ -103,6 +112,27 @@ constexpr uint32_t kBufCols = 128;
 
 __device__ __forceinline__ int slot3(int it) { return it % kRing; }
 __device__ __forceinline__ uint32_t par3(int it) { return (uint32_t)(it / kRing) & 1u; }
+
+// Unit u of the persistent schedule: sequence b, first head h, and g = b H + h,
+// the first head's index in saved_S / dm_unit / saved_norms.  kMerge: a unit
+// is the head pair (h, h + 1).
+struct UnitPos {
+  int b, h, g;
+};
+template <bool kMerge>
+__device__ __forceinline__ UnitPos unit_pos(int u, int H) {
+  const int Hs = kMerge ? H >> 1 : H;
+  UnitPos o;
+  o.b = u / Hs;
+  o.h = (u - o.b * Hs) * (kMerge ? 2 : 1);
+  o.g = o.b * H + o.h;
+  return o;
+}
+// TMA coordinates (column, head) of 32-column box hb of unit position q
+template <bool kMerge>
+__device__ __forceinline__ int box_col(int hb) { return kMerge ? 0 : 32 * hb; }
+template <bool kMerge>
+__device__ __forceinline__ int box_head(const UnitPos& q, int hb) { return kMerge ? q.h + hb : q.h; }
 
 struct Bars {
   uint64_t raw_full[kRing], slot_free[kRing], split_full[kRing], mma_done[kRing], staged[kRing];
@@ -240,14 +270,16 @@ __device__ __forceinline__ void teardown(uint32_t tmem, int warp) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
   }
 }
+template <bool kMerge>
 __device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars* br, int lane) {
   UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
-  const int units = (int)(p.B * p.H), H = (int)p.H;
+  const int H = (int)p.H, Hs = kMerge ? H >> 1 : H;
+  const int units = (int)p.B * Hs;
   int j = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
     const int sl = j & 1;
     mbar_wait(&br->fl_empty[sl], ((j >> 1) & 1) ^ 1);
-    tc::mask_unit(p, u / H, reinterpret_cast<uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8)),
+    tc::mask_unit(p, u / Hs, reinterpret_cast<uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8)),
                   &ucs[sl], lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&br->fl_full[sl]);
@@ -311,6 +343,7 @@ struct SplitRow {
   float x[16];
   float ss;  // |row|^2
 };
+template <bool kMerge = false>
 __device__ __forceinline__ void split_load(const uint8_t* X, int t, SplitRow& s, bool norm) {
   s.row = t >> 2;
   s.q = t & 3;
@@ -331,7 +364,8 @@ __device__ __forceinline__ void split_load(const uint8_t* X, int t, SplitRow& s,
     }
     float part = a + b;
     part += __shfl_xor_sync(0xffffffffu, part, 1);
-    s.ss = part + __shfl_xor_sync(0xffffffffu, part, 2);
+    // kMerge: threads q = 0, 1 hold head h's row, q = 2, 3 head h + 1's
+    s.ss = kMerge ? part : part + __shfl_xor_sync(0xffffffffu, part, 2);
   }
 }
 // The split row's 16 values as parts over its own raw tile: part 0 over box 0,
@@ -346,13 +380,14 @@ __device__ __forceinline__ void split_store(uint8_t* X, uint8_t* P2, const Split
 // ======================================================================================
 // Forward
 // ======================================================================================
+template <bool kMerge>
 __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
     const OpParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = (int)p.N, H = (int)p.H;
-  const int units = (int)(p.B * p.H);
+  const int units = (int)p.B * (kMerge ? H >> 1 : H);
   const int C = (N + kRows - 1) / kRows;
   const int P = (p.out != nullptr || p.saved_norms != nullptr) ? 2 : 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -372,12 +407,12 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
       d32::prefetch_map(&tq);
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int b = u / H, h = u - b * H;
+        const UnitPos up = unit_pos<kMerge>(u, H);
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
             tc::ItemPos f;
-            if (p.l2_ahead && tc::item_pos(it + p.l2_ahead, P, C, units, H, f))
+            if (!kMerge && p.l2_ahead && tc::item_pos(it + p.l2_ahead, P, C, units, H, f))
               for (int hb = 0; hb < 2; ++hb) {  // L2 prefetch of a later item (long N)
                 tc::tma_prefetch_4d(f.ps == 0 ? &tk : &tq, 32 * hb, f.c * kRows, f.h, f.b);
                 if (f.ps == 0) tc::tma_prefetch_4d(&tv, 32 * hb, f.c * kRows, f.h, f.b);
@@ -387,13 +422,16 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
             if (ps == 0) {
               mbar_expect_tx(&br->raw_full[st], 2 * kRaw);
               for (int hb = 0; hb < 2; ++hb) {
-                tma_load_4d(X + hb * kBox, &tk, 32 * hb, c * kRows, h, b, &br->raw_full[st]);
-                tma_load_4d(X + kRaw + hb * kBox, &tv, 32 * hb, c * kRows, h, b, &br->raw_full[st]);
+                tma_load_4d(X + hb * kBox, &tk, box_col<kMerge>(hb), c * kRows, box_head<kMerge>(up, hb), up.b,
+                            &br->raw_full[st]);
+                tma_load_4d(X + kRaw + hb * kBox, &tv, box_col<kMerge>(hb), c * kRows, box_head<kMerge>(up, hb),
+                            up.b, &br->raw_full[st]);
               }
             } else {
               mbar_expect_tx(&br->raw_full[st], kRaw);
               for (int hb = 0; hb < 2; ++hb)
-                tma_load_4d(X + hb * kBox, &tq, 32 * hb, c * kRows, h, b, &br->raw_full[st]);
+                tma_load_4d(X + hb * kBox, &tq, box_col<kMerge>(hb), c * kRows, box_head<kMerge>(up, hb), up.b,
+                            &br->raw_full[st]);
             }
           }
       }
@@ -427,20 +465,20 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
         }
     }
   } else if (warp == kWarpMask) {
-    mask_loop(p, smem, br, lane);
+    mask_loop<kMerge>(p, smem, br, lane);
   } else if (warp == kWarpStore) {
     if (lane == 0) {
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int b = u / H, h = u - b * H;
+        const UnitPos up = unit_pos<kMerge>(u, H);
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
             mbar_wait(&br->staged[st], par3(it));
             if (ps == 1 && p.out) {  // O staged over Y (free in pass 2)
               uint8_t* Y = smem + kOffRing + st * kSlot + kRaw;
-              tma_store_4d(&to, Y, 0, c * kRows, h, b);
-              tma_store_4d(&to, Y + kBox, 32, c * kRows, h, b);
+              tma_store_4d(&to, Y, box_col<kMerge>(0), c * kRows, box_head<kMerge>(up, 0), up.b);
+              tma_store_4d(&to, Y + kBox, box_col<kMerge>(1), c * kRows, box_head<kMerge>(up, 1), up.b);
               bulk_wait_read0();
             }
             mbar_arrive(&br->slot_free[st]);
@@ -460,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int sl = j & 1;
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
-      float* norms = norms_all ? norms_all + (int64_t)u * 2 * N : nullptr;
+      const UnitPos up = unit_pos<kMerge>(u, H);
       mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
       const UnitConst uc = ucs[sl];
       for (int k = 0; k < P * C; ++k, ++it) {
@@ -471,12 +509,16 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
         if (splitter) {  // ---------------- splitter (4 threads per row) ----------------
           mbar_wait(&br->raw_full[st], par3(it));
           SplitRow s;
-          split_load(X, t, s, true);
+          split_load<kMerge>(X, t, s, true);
           const int r = c * kRows + s.row;
           const float iv = rsqrtf(s.ss + eps);
+          // this thread's head (kMerge: q = 2, 3 hold the second head) and its saved norms
+          float* norms = norms_all && r < N && (s.q & (kMerge ? 1 : 3)) == 0
+                             ? norms_all + (int64_t)(up.g + (kMerge ? s.q >> 1 : 0)) * 2 * N
+                             : nullptr;
           if (ps == 0) {  // k~ masked (attention.cpp:334-343), V as it is
             const bool f = r < N && tc::flag_at(fl, r);
-            if (norms && r < N && s.q == 0) norms[N + r] = f ? (s.ss + eps) * iv : 1.0f;
+            if (norms) norms[N + r] = f ? (s.ss + eps) * iv : 1.0f;
 #pragma unroll
             for (int e = 0; e < 16; ++e) s.x[e] = f ? s.x[e] * iv : 0.f;  // NaN-safe zeros
             SplitRow v;
@@ -485,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
             split_store(X, X + 2 * kRaw, s);
             split_store(Y, X + 2 * kRaw + kBox, v);
           } else {  // q~ every row (:366-377)
-            if (norms && r < N && s.q == 0) norms[r] = (s.ss + eps) * iv;
+            if (norms) norms[r] = (s.ss + eps) * iv;
 #pragma unroll
             for (int e = 0; e < 16; ++e) s.x[e] *= iv;
             __syncwarp();
@@ -508,7 +550,25 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
               __syncwarp();
               if (lane == 0) mbar_arrive(&br->acc_free);
             }
-            if (c == C - 1) {  // S complete: saved S + its three part tiles
+            if (kMerge && c == C - 1) {  // the two heads' S: diagonal blocks, operand blockdiag
+              const int hh = wq >> 1;  // rows 0-31: first head (columns 0-31), 32-63: second
+              float sv[32];
+              acc_half(tmem, run, wq, lane, hh, C > kFlush, sv);
+              if (lane < 16) {
+                const int a = 16 * wq + lane;
+                if (gS_all) {
+                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)(up.g + hh) * 1024 + (a & 31) * 32);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e)
+                    gs[e] = make_float4(sv[4 * e], sv[4 * e + 1], sv[4 * e + 2], sv[4 * e + 3]);
+                }
+                float z[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) z[e] = 0.f;
+                store_state_half(ops, a, hh, sv);
+                store_state_half(ops, a, hh ^ 1, z);
+              }
+            } else if (c == C - 1) {  // S complete: saved S + its three part tiles
 #pragma unroll 1
               for (int h = 0; h < 2; ++h) {
                 float sv[32];
@@ -524,6 +584,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
                   store_state_half(ops, a, h, sv);
                 }
               }
+            }
+            if (c == C - 1) {
               fence_proxy_async();
               tc_fence_before();
               epi_sync();
@@ -551,6 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
 // ======================================================================================
 // Backward
 // ======================================================================================
+template <bool kMerge>
 __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
@@ -558,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
     const __grid_constant__ CUtensorMap tdv, const OpParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = (int)p.N, H = (int)p.H;
-  const int units = (int)(p.B * p.H);
+  const int units = (int)p.B * (kMerge ? H >> 1 : H);
   const int C = (N + kRows - 1) / kRows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
@@ -580,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
       d32::prefetch_map(&tv);
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int b = u / H, h = u - b * H;
+        const UnitPos up = unit_pos<kMerge>(u, H);
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
@@ -588,9 +651,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
             uint8_t* X = smem + kOffRing + st * kSlot;
             mbar_expect_tx(&br->raw_full[st], 2 * kRaw);
             for (int hb = 0; hb < 2; ++hb) {
-              tma_load_4d(X + hb * kBox, ps == 0 ? &tq : &tk, 32 * hb, c * kRows, h, b, &br->raw_full[st]);
-              tma_load_4d(X + kRaw + hb * kBox, ps == 0 ? &tdo : &tv, 32 * hb, c * kRows, h, b,
-                          &br->raw_full[st]);
+              tma_load_4d(X + hb * kBox, ps == 0 ? &tq : &tk, box_col<kMerge>(hb), c * kRows,
+                          box_head<kMerge>(up, hb), up.b, &br->raw_full[st]);
+              tma_load_4d(X + kRaw + hb * kBox, ps == 0 ? &tdo : &tv, box_col<kMerge>(hb), c * kRows,
+                          box_head<kMerge>(up, hb), up.b, &br->raw_full[st]);
             }
           }
       }
@@ -632,25 +696,25 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
         }
     }
   } else if (warp == kWarpMask) {
-    mask_loop(p, smem, br, lane);
+    mask_loop<kMerge>(p, smem, br, lane);
   } else if (warp == kWarpStore) {
     if (lane == 0) {
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int b = u / H, h = u - b * H;
+        const UnitPos up = unit_pos<kMerge>(u, H);
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
             uint8_t* X = smem + kOffRing + st * kSlot;
             mbar_wait(&br->staged[st], par3(it));
-            if (ps == 0) {
-              tma_store_4d(&tdq, X, 0, c * kRows, h, b);
-              tma_store_4d(&tdq, X + kBox, 32, c * kRows, h, b);
-            } else {
-              tma_store_4d(&tdk, X, 0, c * kRows, h, b);
-              tma_store_4d(&tdk, X + kBox, 32, c * kRows, h, b);
-              tma_store_4d(&tdv, X + kRaw, 0, c * kRows, h, b);
-              tma_store_4d(&tdv, X + kRaw + kBox, 32, c * kRows, h, b);
+            for (int hb = 0; hb < 2; ++hb) {
+              const int bc = box_col<kMerge>(hb), bh = box_head<kMerge>(up, hb);
+              if (ps == 0) {
+                tma_store_4d(&tdq, X + hb * kBox, bc, c * kRows, bh, up.b);
+              } else {
+                tma_store_4d(&tdk, X + hb * kBox, bc, c * kRows, bh, up.b);
+                tma_store_4d(&tdv, X + kRaw + hb * kBox, bc, c * kRows, bh, up.b);
+              }
             }
             bulk_wait_read0();
             mbar_arrive(&br->slot_free[st]);
@@ -670,6 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int sl = j & 1;
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
+      const UnitPos up = unit_pos<kMerge>(u, H);
       mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
       const UnitConst uc = ucs[sl];
       for (int k = 0; k < 2 * C; ++k, ++it) {
@@ -679,18 +744,22 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
         uint8_t* Y = X + kRaw;
         uint8_t* X2 = X + 2 * kRaw;
         uint8_t* Y2 = X2 + kBox;
-        float* inv_st = invs + st * kRows;
+        float* inv_st = invs + st * 2 * kRows;  // [row][half] (kMerge: one per head)
         if (splitter) {  // ---------------- splitter (4 threads per row) ----------------
           if (ps == 0 && c == 0) {
             // this unit's S (saved by the forward) as three part tiles; the previous
             // unit's dQ~ MMAs and G-epilogue (dm) have read its S (op_ready)
             if (j > 0) mbar_wait(&br->op_ready, (j - 1) & 1);
             const int a = t >> 2, q4 = t & 3;  // row a, columns 16 q4 .. 16 q4 + 15
-            const float4* gs = reinterpret_cast<const float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 16 * q4);
+            // kMerge: blockdiag(S_h, S_h+1) — columns 0-31 of rows 0-31 and 32-63 of rows 32-63
+            const bool live = !kMerge || (q4 >> 1) == (a >> 5);
+            const float4* gs = reinterpret_cast<const float4*>(
+                kMerge ? gS_all + (int64_t)(up.g + (a >> 5)) * 1024 + (a & 31) * 32 + 16 * (q4 & 1)
+                       : gS_all + (int64_t)u * 4096 + a * 64 + 16 * q4);
             float vv[16];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float4 v = __ldg(gs + e);
+              const float4 v = live ? __ldg(gs + e) : make_float4(0.f, 0.f, 0.f, 0.f);
               vv[4 * e] = v.x;
               vv[4 * e + 1] = v.y;
               vv[4 * e + 2] = v.z;
@@ -701,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
           }
           mbar_wait(&br->raw_full[st], par3(it));
           SplitRow s, y;
-          split_load(X, t, s, true);
+          split_load<kMerge>(X, t, s, true);
           split_load(Y, t, y, false);
           const int r = c * kRows + s.row;
           const float iv = rsqrtf(s.ss + eps);
@@ -714,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
 #pragma unroll
             for (int e = 0; e < 16; ++e) s.x[e] = f ? s.x[e] * iv : 0.f;
           }
-          if (s.q == 0) inv_st[s.row] = iv;  // 1/norm for the epiloguer's Jacobian
+          if ((s.q & (kMerge ? 1 : 3)) == 0) inv_st[2 * s.row + (s.q >> 1)] = iv;  // for the Jacobian
           __syncwarp();
           split_store(X, X2, s);
           split_store(Y, Y2, y);
@@ -729,8 +798,16 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
             float dotf = 0.f;
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
+              // kMerge: only the diagonal blocks (rows 0-31 x columns 0-31: the first
+              // head's G, rows 32-63 x columns 32-63: the second's); the operand is
+              // blockdiag(s G_h, s G_h+1)
+              const bool live = !kMerge || h == (wq >> 1);
               float gr[32];
               acc_half(tmem, run, wq, lane, h, C > kFlush, gr);
+              if (!live) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) gr[e] = 0.f;
+              }
               if (lane < 16) {
                 const int a = 16 * wq + lane;
 #pragma unroll
@@ -753,8 +830,15 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
             tc_fence_before();
             epi_sync();
             if (t == 0) {
-              const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
-              if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
+              if (kMerge) {  // one dm per head: warps 0-1 hold the first head's rows
+                if (p.dm_unit) {
+                  p.dm_unit[up.g] = uc.coef * (dm_x[0] + dm_x[1]);
+                  p.dm_unit[up.g + 1] = uc.coef * (dm_x[2] + dm_x[3]);
+                }
+              } else {
+                const double dsum = ((dm_x[0] + dm_x[1]) + dm_x[2]) + dm_x[3];
+                if (p.dm_unit) p.dm_unit[u] = uc.coef * dsum;
+              }
               mbar_arrive(&br->op_ready);
             }
           }
@@ -768,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
           }
           const int row = 16 * wq + (lane & 15), h = lane >> 4;
           const int r = c * kRows + row;
-          const float iv = inv_st[row];
+          const float iv = inv_st[2 * row + (kMerge ? h : 0)];
           const uint32_t D = tmem + kBuf0 + kBufCols * st + lane_base;
           // g = dQ~ or dK~ (this thread's 32 columns), x~ = the part tiles rebuilt
           float g[32], x[32];
@@ -778,7 +862,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
           float pr = 0.f;
 #pragma unroll
           for (int e = 0; e < 32; ++e) pr = fmaf(g[e], x[e], pr);
-          pr += __shfl_xor_sync(0xffffffffu, pr, 16);  // the row's other half
+          const float pr_other = __shfl_xor_sync(0xffffffffu, pr, 16);  // the row's other half
+          if (!kMerge) pr += pr_other;  // kMerge: each half is its own head's row
           __syncwarp();  // both halves have read the parts of X before they are overwritten
           if (ps == 0) {
             // dQ_i = (g - (g.q~_i) q~_i) / nq_i, g = s dO S^T (:410-411, :421-428); staged over X
@@ -825,18 +910,20 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
   }
   if (threadIdx.x == 32 * kWarpEpi0 && p.dm_total) __threadfence();
   teardown(tmem, warp);
-  if (p.dm_total) tc::last_cta_dm_total(p, units, smem + kOffRing);
+  if (p.dm_total) tc::last_cta_dm_total(p, (int)(p.B * p.H), smem + kOffRing);
 }
 
 }  // namespace tcf
 
 // ---- host side ----------------------------------------------------------------------
 
-// 4-D fp32 map over (D, N, H, B), box (32, 64, 1, 1), 128-byte swizzle.
+// 4-D fp32 map over (D, N, H, B), box (32, 64, 1, 1), 128-byte swizzle
+// (d_h = 64: two boxes per row; head-merged d_h = 32: one box per head).
+inline bool tcf_merge(const OpParams& p) { return p.D == 32; }
 inline bool make_tcf_map(CUtensorMap* map, const void* base, const OpParams& p) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[4] = {64, (cuuint64_t)p.N, (cuuint64_t)p.H, (cuuint64_t)p.B};
+  cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)p.N, (cuuint64_t)p.H, (cuuint64_t)p.B};
   cuuint64_t strides[3] = {(cuuint64_t)p.sn * 4, (cuuint64_t)p.sh * 4, (cuuint64_t)p.sb * 4};
   cuuint32_t box[4] = {32, (cuuint32_t)tcf::kRows, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
@@ -845,7 +932,12 @@ inline bool make_tcf_map(CUtensorMap* map, const void* base, const OpParams& p) 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 inline bool tcf_layout_ok(const OpParams& p, std::initializer_list<const void*> ptrs) {
-  if (p.D != 64 || p.N < 1 || p.N > tcf::kMaxN) return false;
+  if (p.N < 1 || p.N > tcf::kMaxN) return false;
+  if (p.D == 32) {  // head-merged: short sequences (one 64-row chunk holds both heads' rows)
+    if (p.N > tcf::kRows || (p.H & 1) || getenv("COTTEN_NO_TCF_MERGE")) return false;
+  } else if (p.D != 64) {
+    return false;
+  }
   if ((p.sn * 4) % 16 || (p.sh * 4) % 16 || (p.sb * 4) % 16) return false;
   if (p.B * p.H > (1ll << 31) - 1) return false;
   for (const void* q : ptrs)
@@ -888,13 +980,14 @@ inline int launch_tcf_fwd(const OpParams& p, cudaStream_t st) {
   if (!make_tcf_map(&mq, p.q, p) || !make_tcf_map(&mk, p.k, p) || !make_tcf_map(&mv, p.v, p) ||
       !make_tcf_map(&mo, p.out ? p.out : p.q, p))
     return -1;
-  if (cudaFuncSetAttribute(tcf::cos_fwd_tcf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)tcf::kSmemBytes) != cudaSuccess)
+  auto kern = tcf_merge(p) ? tcf::cos_fwd_tcf_kernel<true> : tcf::cos_fwd_tcf_kernel<false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcf::kSmemBytes) !=
+      cudaSuccess)
     return -1;
-  const int grid = std::min((int)(p.B * p.H), sm_count());
+  const int grid = std::min((int)(p.B * p.H / (tcf_merge(p) ? 2 : 1)), sm_count());
   OpParams q = p;
   q.l2_ahead = l2_ahead_items(true, (int)((p.N + tcf::kRows - 1) / tcf::kRows));
-  if (launch_tcf_pdl(tcf::cos_fwd_tcf_kernel, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
+  if (launch_tcf_pdl(kern, grid, st, mq, mk, mv, mo, q) != cudaSuccess) return -1;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 inline int launch_tcf_bwd(const OpParams& p, cudaStream_t st) {
@@ -903,12 +996,12 @@ inline int launch_tcf_bwd(const OpParams& p, cudaStream_t st) {
       !make_tcf_map(&mg, p.dout, p) || !make_tcf_map(&mdq, p.dq, p) || !make_tcf_map(&mdk, p.dk, p) ||
       !make_tcf_map(&mdv, p.dv, p))
     return -1;
-  if (cudaFuncSetAttribute(tcf::cos_bwd_tcf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)tcf::kSmemBytes) != cudaSuccess)
-    return -1;
-  const int grid = std::min((int)(p.B * p.H), sm_count());
-  if (launch_tcf_pdl(tcf::cos_bwd_tcf_kernel, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, p) !=
+  auto kern = tcf_merge(p) ? tcf::cos_bwd_tcf_kernel<true> : tcf::cos_bwd_tcf_kernel<false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcf::kSmemBytes) !=
       cudaSuccess)
+    return -1;
+  const int grid = std::min((int)(p.B * p.H / (tcf_merge(p) ? 2 : 1)), sm_count());
+  if (launch_tcf_pdl(kern, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, p) != cudaSuccess)
     return -1;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

@@ -152,7 +152,20 @@ def test_seq_len_edges_f32(N, flags):
     h = inputs.make_host(B, H, N, D, seed=N)
     valid = inputs.left_padded_mask(B, N, N)
     res = run_gpu(h, valid, 0.75, 1e-6, "f32", flags)
-    assert_parity(res, oracle_for(res["inputs"], valid, 0.75, 1e-6), valid, "f32")
+    ref = oracle_for(res["inputs"], valid, 0.75, 1e-6)
+    if N <= 3:
+        # one to three rows: O = s (q~.k~) v cancels, so the error is bounded
+        # against the magnitude evaluated on absolute values (the stated rule of
+        # test_gpu_schedule.py::test_tiny_sequences_seed_sweep)
+        from test_gpu_schedule import _abs_scales
+        sc = _abs_scales(res["inputs"], valid, 0.75, 1e-6)
+        for name, want in zip(("out", "dq", "dk", "dv"), ref[:4]):
+            err = np.abs(res[name] - want).reshape(B * H, -1).max(1) / np.maximum(sc[name], 1e-30)
+            assert err.max() <= 1e-5, (name, float(err.max()))
+        pad = np.broadcast_to((valid == 0)[:, None, :], (B, H, N))
+        assert np.all(res["dk"][pad] == 0.0) and np.all(res["dv"][pad] == 0.0)
+    else:
+        assert_parity(res, ref, valid, "f32")
 
 
 @pytest.mark.parametrize("D", [1, 2, 3, 5, 8, 16, 24, 32, 48, 64, 96, 128])
