@@ -250,6 +250,17 @@ __device__ __forceinline__ void bulk_wait_read0() {
 __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+// End of a store warp: every store was followed by bulk_wait_read0 (its
+// shared-memory source is read), and the global writes complete with the
+// grid — as CUTLASS's TMA epilogues rely on (their tail wait is the .read
+// form) — so the CTA does not hold its exit for them (the backward's last
+// dK / dV stores kept CTAs ~2 us past their last item at ML-1M).
+#ifndef COTTEN_TAIL_FULL_WAIT
+#define COTTEN_TAIL_FULL_WAIT 0
+#endif
+__device__ __forceinline__ void store_tail() {
+  if (COTTEN_TAIL_FULL_WAIT) bulk_wait0();
+}
 
 // ---- row access in a 128B-swizzled 128-row tile -----------------------------
 
@@ -954,7 +965,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
             mbar_arrive(&br->lo_free[bf]);
           }
       }
-      bulk_wait0();
+      store_tail();
     }
   } else {
     // ===== workers: group 0 splits every chunk, group 1 runs every epilogue;
@@ -1021,7 +1032,9 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
               // a pass-1 item stages nothing and its MMAs are done: release the slot
               // before the flush / S-epilogue, which work in TMEM and the operand
               // area only (the splitter may refill the slot meanwhile)
+              TC_TRACE(5);
               arrive_staged(br, bf, lane);
+              TC_TRACE(4);
               uint8_t* run = ops + 2 * kOpBytes;  // 8 KB the forward does not otherwise use
               uint8_t* scr = ops + 4 * kOpBytes;  // and 8 KB more: the S-epilogue's scratch
               if (c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
@@ -1180,7 +1193,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             mbar_arrive(&br->lo_free[bf]);
           }
       }
-      bulk_wait0();
+      store_tail();
     }
   } else {
     // ===== workers: group 0 splits every chunk, group 1 runs every epilogue =====

@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
             TCB_TRACE(7, true);
           }
       }
-      bulk_wait0();
+      tc::store_tail();
     }
   } else {
     const bool splitter = warp < kWarpEpi0;
@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
             TCB_TRACE(7, true);
           }
       }
-      bulk_wait0();
+      tc::store_tail();
     }
   } else {
     const bool splitter = warp < kWarpEpi0;

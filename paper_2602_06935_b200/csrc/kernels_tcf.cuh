@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
             mbar_arrive(&br->slot_free[st]);
           }
       }
-      bulk_wait0();
+      tc::store_tail();
     }
   } else {
     const bool splitter = warp < kWarpEpi0;
@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
             mbar_arrive(&br->slot_free[st]);
           }
       }
-      bulk_wait0();
+      tc::store_tail();
     }
   } else {
     const bool splitter = warp < kWarpEpi0;

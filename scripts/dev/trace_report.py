@@ -50,3 +50,21 @@ for tag in ("fwd", "bwd"):
     c = (c - t0) / 1e3  # us
     print(f"{tag} CTA timeline (us from the first CTA entry): entry max {c[:, 0].max():.2f}  setup done mean {c[:, 1].mean():.2f}"
           f"  last item done mean {c[:, 2].mean():.2f} max {c[:, 2].max():.2f}  exit max {c[:, 3].max():.2f}")
+
+# Item timeline of the slowest CTA (clock64 cycles from its first splitter stamp, in us at 1.965 GHz)
+for tag in ("fwd", "bwd"):
+    try:
+        a = np.fromfile(f"{sys.argv[1]}/{tag}.bin", dtype=np.int64).reshape(-1, 3, K, 8)
+    except FileNotFoundError:
+        continue
+    c = a[:, 2, K - 1, 4:8].astype(np.float64)
+    live = np.where(c[:, 0] > 0)[0]
+    slow = live[np.argmax(c[live, 2])]
+    sp, ep, mm = (a[slow, i].astype(np.float64) for i in range(3))
+    n = int(((sp[:, 0] > 0) & (sp[:, 2] > 0)).sum())
+    t0 = sp[0, 0]
+    us = lambda x: (x - t0) / 1965.0  # noqa: E731
+    print(f"{tag}: slowest CTA {slow}, {n} items (us): split start / published | mma start / issued | epi sees done / staged")
+    for it in range(min(n, 24)):
+        print(f"  it {it:2d}: {us(sp[it, 1]):6.2f} {us(sp[it, 2]):6.2f} | {us(mm[it, 1]):6.2f} {us(mm[it, 2]):6.2f} | "
+              f"{us(ep[it, 3]):6.2f} {us(ep[it, 4]):6.2f}")
