@@ -228,6 +228,28 @@ __device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, 
       "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// L2 prefetch of a contiguous global range (bytes: a multiple of 16).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)),
+               "r"(bytes)
+               : "memory");
+}
+// A/B switches of the start-up and ring-release schedule (profiles/)
+#ifndef COTTEN_ISSUED_GATE
+#define COTTEN_ISSUED_GATE 0  // measured: ML-20M bwd 0.757 -> 0.735 with it (profiles/r02s_start)
+#endif
+#ifndef COTTEN_WARM_L2
+#define COTTEN_WARM_L2 1
+#endif
+#ifndef COTTEN_EARLY_RAW_RELEASE
+#define COTTEN_EARLY_RAW_RELEASE 1
+#endif
+// Per-line L2 prefetch of a global range (any alignment).
+__device__ __forceinline__ void prefetch_l2_lines(const void* src, int64_t bytes) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(127);
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(src) + bytes;
+  for (uintptr_t a = a0; a < a1; a += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
 // The chunk item `it` of this CTA's persistent schedule (units blockIdx.x +
 // j gridDim.x, each P passes x C chunks): false past the last unit.
 struct ItemPos {
@@ -250,13 +272,12 @@ __device__ __forceinline__ void bulk_wait_read0() {
 __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
-// End of a store warp: every store was followed by bulk_wait_read0 (its
-// shared-memory source is read), and the global writes complete with the
-// grid — as CUTLASS's TMA epilogues rely on (their tail wait is the .read
-// form) — so the CTA does not hold its exit for them (the backward's last
-// dK / dV stores kept CTAs ~2 us past their last item at ML-1M).
+// End of a store warp: every store was already followed by bulk_wait_read0
+// (its shared-memory source is read); the full wait for the global writes is
+// kept (COTTEN_TAIL_FULL_WAIT=0 — exiting without it, as CUTLASS's TMA
+// epilogues do — measured neutral at ML-1M / ML-20M, profiles/r02r_tail).
 #ifndef COTTEN_TAIL_FULL_WAIT
-#define COTTEN_TAIL_FULL_WAIT 0
+#define COTTEN_TAIL_FULL_WAIT 1
 #endif
 __device__ __forceinline__ void store_tail() {
   if (COTTEN_TAIL_FULL_WAIT) bulk_wait0();
@@ -494,8 +515,11 @@ __device__ __noinline__ void unit_scale(double m, int n, float* s_out, double* c
 }
 
 // Bitmask of valid rows + true_n + the fp64 scale constants of unit (b).
+// `issued` (first unit only): arrived on once this warp's first valid-byte
+// loads are issued, before their values are used — the producer holds its
+// first TMA loads for it (see Bars::issued).
 __device__ __forceinline__ void mask_unit(const OpParams& p, int64_t b, uint32_t* fl,
-                                          UnitConst* uc, int lane) {
+                                          UnitConst* uc, int lane, uint64_t* issued = nullptr) {
   const int N = (int)p.N;
   const int words = (N + 31) >> 5;
   int cnt = 0;
@@ -506,6 +530,11 @@ __device__ __forceinline__ void mask_unit(const OpParams& p, int64_t b, uint32_t
     for (int k = 0; k < 8; ++k) {  // 8 loads in flight before the first ballot
       const int r = (w0 + k) * 32 + lane;
       v[k] = (w0 + k < words && r < N) ? (row ? __ldg(row + r) : (uint8_t)1) : (uint8_t)0;
+    }
+    if (issued) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(issued);
+      issued = nullptr;
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -626,7 +655,22 @@ constexpr int kTraceItems = 64;
           (long long)gt_;                                                                 \
     }                                                                                     \
   } while (0)
+// Start-up stamps (globaltimer ns) at [cta][2][kTraceItems-2][k]: 0 mask warp after
+// its first loads are issued, 1 its flags published (fl_full), 2 producer's first TMA
+// issued, 3 splitter passed fl_full, 4 splitter saw item 0 land.
+#define TC_TRACE_T0(k)                                                                    \
+  do {                                                                                    \
+    if (p.workspace) {                                                                    \
+      unsigned long long gt_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                              \
+      static_cast<long long*>(p.workspace)[((blockIdx.x * 3 + 2) * kTraceItems + kTraceItems - 2) * 8 + (k)] = \
+          (long long)gt_;                                                                 \
+    }                                                                                     \
+  } while (0)
 #else
+#define TC_TRACE_T0(k) \
+  do {                 \
+  } while (0)
 #define TC_TRACE_CTA(k) \
   do {                  \
   } while (0)
@@ -649,6 +693,11 @@ struct Bars {
   uint64_t red_done;                    // bwd: a unit's G reduction MMAs complete (per unit)
   uint64_t fl_full[2], fl_empty[2];     // mask warp <-> workers (slot = unit & 1)
   uint64_t staged[kRing], lo_free[kRing];  // epiloguer -> store warp -> splitter
+  // The first unit's small dependent loads (valid bytes; bwd: saved S) are
+  // issued before the producer's first TMA loads: at a kernel start all 148
+  // CTAs request three ring slots at once (~14 MB, ~2 us of HBM), and a mask
+  // load queued behind them held the first split ~4 us at ML-1M (trace).
+  uint64_t issued;
 };
 static_assert(sizeof(Bars) <= 256, "barrier area");
 
@@ -657,7 +706,8 @@ __device__ __forceinline__ void group_sync(int g) {
 }
 
 // Barrier init + TMEM allocation (256 columns, one CTA per SM).
-__device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* tslot, int warp) {
+__device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* tslot, int warp,
+                                             int issued_count) {
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
     for (int i = 0; i < kRing; ++i) {
@@ -675,6 +725,7 @@ __device__ __forceinline__ uint32_t tc_setup(uint8_t* smem, Bars* br, uint32_t* 
     mbar_init(&br->op_ready, 1);
     mbar_init(&br->acc_free, 4);
     mbar_init(&br->red_done, 1);
+    mbar_init(&br->issued, issued_count);
     d32::fence_barrier_init();
   }
   if (warp == kWarpMma) {
@@ -741,10 +792,12 @@ __device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars
   for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
     const int sl = j & 1;
     mbar_wait(&br->fl_empty[sl], ((j >> 1) & 1) ^ 1);
+    if (lane == 0 && j == 0) TC_TRACE_T0(0);
     mask_unit(p, u / H, reinterpret_cast<uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8)),
-              &ucs[sl], lane);
+              &ucs[sl], lane, j == 0 ? &br->issued : nullptr);
     __syncwarp();
     if (lane == 0) mbar_arrive(&br->fl_full[sl]);
+    if (lane == 0 && j == 0) TC_TRACE_T0(1);
   }
 }
 
@@ -876,7 +929,27 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
   UnitConst* ucs = reinterpret_cast<UnitConst*>(smem + kOffMisc);
   uint8_t* ops = smem + kOffOps;
   if (threadIdx.x == 0) TC_TRACE_CTA(4);
-  const uint32_t tmem = tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
+  const uint32_t tmem =
+      tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp, 1);
+  // Before the dependency resolves: warm L2 with this CTA's first three items and its
+  // first two units' valid bytes.  A prefetch is only a hint (if the preceding kernel
+  // still writes these lines, the loads after pdl_wait read its data from L2); it
+  // overlaps the first HBM round trip (~2 us at a cold start, trace) with that
+  // kernel's tail.
+  if (COTTEN_WARM_L2 && warp == kWarpProducer && lane == 0) {
+    for (int it = 0; it < kRing; ++it) {
+      ItemPos f;
+      if (!item_pos(it, P, C, units, H, f)) break;
+      if (f.ps == 0) {
+        tma_prefetch_4d(&tk, 0, f.c * kRows, f.h, f.b);
+        tma_prefetch_4d(&tv, 0, f.c * kRows, f.h, f.b);
+      } else {
+        tma_prefetch_4d(&tq, 0, f.c * kRows, f.h, f.b);
+      }
+    }
+    for (int u = blockIdx.x; p.valid && u < units && u < (int)blockIdx.x + 2 * (int)gridDim.x; u += gridDim.x)
+      prefetch_l2_lines(p.valid + (int64_t)(u / H) * p.msb, N);
+  }
   pdl_wait();
   const KernelStamp stamp_(p);
   pdl_launch_dependents();
@@ -893,6 +966,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            if (COTTEN_ISSUED_GATE && it == 0) mbar_wait(&br->issued, 0);  // mask loads go first
             ItemPos f;
             if (p.l2_ahead && item_pos(it + p.l2_ahead, P, C, units, H, f)) {
               if (f.ps == 0) {
@@ -908,6 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
               mbar_expect_tx(&br->raw_full[st], 2 * kTile);
               tma_load_4d(dst, &tk, 0, c * kRows, h, b, &br->raw_full[st]);
               tma_load_4d(dst + kTile, &tv, 0, c * kRows, h, b, &br->raw_full[st]);
+              if (it == 0) TC_TRACE_T0(2);
             } else {
               mbar_expect_tx(&br->raw_full[st], kTile);
               tma_load_4d(dst, &tq, 0, c * kRows, h, b, &br->raw_full[st]);
@@ -941,7 +1016,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
               issue_rowout_ts<true>(D, D + 32, base + kOffOps, base + kOffOps + kOpBytes);
             }
             TC_TRACE_MMA(2);
-            mma_commit(&br->raw_empty[st]);
+            // pass 2 reads Q~ from TMEM only: the splitter released its raw stage
+            if (ps == 0 || !COTTEN_EARLY_RAW_RELEASE) mma_commit(&br->raw_empty[st]);
             mma_commit(&br->mma_done[bf]);
           }
           __syncwarp();
@@ -992,9 +1068,11 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
           const uint32_t D = tmem + kFwdBuf0 + kFwdBufCols * bf + lane_base;
           if (g == 0) {  // ---------------- splitter ----------------
             TC_TRACE(0);
+            if (it == 0 && t == 0) TC_TRACE_T0(3);
             mbar_wait(&br->raw_full[st], par3(it));
             mbar_wait(&br->lo_free[bf], par3(it) ^ 1u);
             TC_TRACE(1);
+            if (it == 0 && t == 0) TC_TRACE_T0(4);
             if (ps == 0) {  // K~ (masked, attention.cpp:334-343) and V, 32-byte-granule tiles
               float kx[32], vx[32], hh[32], ll[32];
               load_row32_raw(X, t, kx);  // lane order: only re-stored in the same layout
@@ -1012,7 +1090,14 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tc_kernel(
             } else {  // Q~ for every row (attention.cpp:366-377), TMEM A operand of O = Q~ S
               float qx[32];
               load_row(X, t, qx);
-              const float ss = sumsq(qx) + eps;
+              const float ss = sumsq(qx) + eps;  // (every loaded value consumed here)
+              // the raw Q tile is read only here (the MMA takes Q~ from TMEM): release the
+              // stage now, not after the MMA, so the producer's next load starts earlier
+              if (COTTEN_EARLY_RAW_RELEASE) {
+                fence_proxy_async();
+                group_sync(g);
+                if (t == 0) mbar_arrive(&br->raw_empty[st]);
+              }
               const float iv = rsqrtf(ss);
               scale32(qx, iv);
               if (norms && r < N) norms[r] = ss * iv;
@@ -1100,7 +1185,21 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
   double* dm_x = reinterpret_cast<double*>(smem + kOffMisc + 40);
   uint8_t* ops = smem + kOffOps;
   if (threadIdx.x == 0) TC_TRACE_CTA(4);
-  const uint32_t tmem = tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp);
+  const uint32_t tmem =
+      tc_setup(smem, br, reinterpret_cast<uint32_t*>(smem + kOffMisc + 32), warp, 1 + 4);
+  // Warm L2 before the dependency resolves (see the forward): the first three items,
+  // the first two units' valid bytes and the first unit's saved S.
+  if (COTTEN_WARM_L2 && warp == kWarpProducer && lane == 0) {
+    for (int it = 0; it < kRing; ++it) {
+      ItemPos f;
+      if (!item_pos(it, 2, C, units, H, f)) break;
+      tma_prefetch_4d(f.ps == 0 ? &tq : &tk, 0, f.c * kRows, f.h, f.b);
+      tma_prefetch_4d(f.ps == 0 ? &tdo : &tv, 0, f.c * kRows, f.h, f.b);
+    }
+    for (int u = blockIdx.x; p.valid && u < units && u < (int)blockIdx.x + 2 * (int)gridDim.x; u += gridDim.x)
+      prefetch_l2_lines(p.valid + (int64_t)(u / H) * p.msb, N);
+    bulk_prefetch_l2(static_cast<const float*>(p.saved_S) + (int64_t)blockIdx.x * 1024, 4096);
+  }
   pdl_wait();
   const KernelStamp stamp_(p);
   pdl_launch_dependents();
@@ -1118,6 +1217,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            if (COTTEN_ISSUED_GATE && it == 0) mbar_wait(&br->issued, 0);  // mask, S loads go first
             ItemPos f;
             if (p.l2_ahead && item_pos(it + p.l2_ahead, 2, C, units, H, f)) {
               tma_prefetch_4d(f.ps == 0 ? &tq : &tk, 0, f.c * kRows, f.h, f.b);
@@ -1128,6 +1228,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
             mbar_expect_tx(&br->raw_full[st], 2 * kTile);
             tma_load_4d(dst, ps == 0 ? &tq : &tk, 0, c * kRows, h, b, &br->raw_full[st]);
             tma_load_4d(dst + kTile, ps == 0 ? &tdo : &tv, 0, c * kRows, h, b, &br->raw_full[st]);
+            if (it == 0) TC_TRACE_T0(2);
           }
       }
     }
@@ -1210,7 +1311,11 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
         snext[1] = __ldg(gs + t + 128);
       }
     };
-    if (g == 0) fetch_S(blockIdx.x);
+    if (g == 0) {
+      fetch_S(blockIdx.x);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&br->issued);
+    }
     const float qnan = __int_as_float(0x7fc00000);
     int it = 0, j = 0, n_tr = 0;
     (void)n_tr;
@@ -1229,9 +1334,11 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tc_kernel(
           const uint32_t tinv = tmem + kBwdInv + bf + lane_base;
           if (g == 0) {  // ---------------- splitter ----------------
             TC_TRACE(0);
+            if (it == 0 && t == 0) TC_TRACE_T0(3);
             mbar_wait(&br->raw_full[st], par3(it));
             mbar_wait(&br->lo_free[bf], par3(it) ^ 1u);
             TC_TRACE(1);
+            if (it == 0 && t == 0) TC_TRACE_T0(4);
             if (ps == 0) {
               // Q~ every row (:366-377, used again in :421-428); rows past N are exact
               // zeros in G even for eps = 0.  Tiles use the 32-byte-granule swizzle.

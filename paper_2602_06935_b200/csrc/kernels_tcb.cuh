@@ -132,6 +132,7 @@ struct Bars {
   uint64_t raw_full[kRing], slot_free[kRing], split_full[kRing], mma_done[kRing], staged[kRing];
   uint64_t op_ready, acc_free, red_done;
   uint64_t fl_full[2], fl_empty[2];
+  uint64_t issued;  // the first unit's mask loads are out (kernels_tc.cuh Bars::issued)
 };
 static_assert(sizeof(Bars) <= 256, "barrier area");
 
@@ -294,6 +295,7 @@ __device__ __forceinline__ uint32_t setup(uint8_t* smem, Bars* br, uint32_t* tsl
     mbar_init(&br->op_ready, 1);
     mbar_init(&br->acc_free, kEpiWarps);
     mbar_init(&br->red_done, 1);
+    mbar_init(&br->issued, 1);
     d32::fence_barrier_init();
   }
   if (warp == kWarpMma) {
@@ -322,7 +324,7 @@ __device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars
     const int sl = j & 1;
     mbar_wait(&br->fl_empty[sl], ((j >> 1) & 1) ^ 1);
     tc::mask_unit(p, u / H, reinterpret_cast<uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8)),
-                  &ucs[sl], lane);
+                  &ucs[sl], lane, j == 0 ? &br->issued : nullptr);
     __syncwarp();
     if (lane == 0) mbar_arrive(&br->fl_full[sl]);
   }
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            if (COTTEN_ISSUED_GATE && it == 0) mbar_wait(&br->issued, 0);  // mask loads go first
             tc::ItemPos f;
             if (p.l2_ahead && tc::item_pos(it + p.l2_ahead, P, C, units, H, f)) {
               if (f.ps == 0) {
@@ -691,11 +694,17 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
       d32::prefetch_map(&tk);
       d32::prefetch_map(&tv);
       int it = 0;
+      const int64_t sbytes = (int64_t)p.D * p.D * 4;  // one unit's saved S
+      if (blockIdx.x < units) tc::bulk_prefetch_l2(static_cast<const uint8_t*>(p.saved_S) + blockIdx.x * sbytes, (uint32_t)sbytes);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = u / H, h = u - b * H;
+        // the splitter loads the next unit's S at its first chunk: have it in L2
+        if (u + (int)gridDim.x < units)
+          tc::bulk_prefetch_l2(static_cast<const uint8_t*>(p.saved_S) + (u + gridDim.x) * sbytes, (uint32_t)sbytes);
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            if (COTTEN_ISSUED_GATE && it == 0) mbar_wait(&br->issued, 0);  // mask loads go first
             tc::ItemPos f;
             if (p.l2_ahead && tc::item_pos(it + p.l2_ahead, 2, C, units, H, f)) {
               tc::tma_prefetch_4d(f.ps == 0 ? &tq : &tk, 0, f.c * kRows, f.h, f.b);

@@ -138,6 +138,7 @@ struct Bars {
   uint64_t raw_full[kRing], slot_free[kRing], split_full[kRing], mma_done[kRing], staged[kRing];
   uint64_t op_ready, acc_free, red_done;
   uint64_t fl_full[2], fl_empty[2];
+  uint64_t issued;  // the first unit's mask loads are out (kernels_tc.cuh Bars::issued)
 };
 static_assert(sizeof(Bars) <= 256, "barrier area");
 
@@ -250,6 +251,7 @@ __device__ __forceinline__ uint32_t setup(uint8_t* smem, Bars* br, uint32_t* tsl
     mbar_init(&br->op_ready, 1);
     mbar_init(&br->acc_free, kEpiWarps);
     mbar_init(&br->red_done, 1);
+    mbar_init(&br->issued, 1);
     d32::fence_barrier_init();
   }
   if (warp == kWarpMma) {
@@ -280,7 +282,7 @@ __device__ __forceinline__ void mask_loop(const OpParams& p, uint8_t* smem, Bars
     const int sl = j & 1;
     mbar_wait(&br->fl_empty[sl], ((j >> 1) & 1) ^ 1);
     tc::mask_unit(p, u / Hs, reinterpret_cast<uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8)),
-                  &ucs[sl], lane);
+                  &ucs[sl], lane, j == 0 ? &br->issued : nullptr);
     __syncwarp();
     if (lane == 0) mbar_arrive(&br->fl_full[sl]);
   }
@@ -411,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
         for (int ps = 0; ps < P; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            if (COTTEN_ISSUED_GATE && it == 0) mbar_wait(&br->issued, 0);  // mask loads go first
             tc::ItemPos f;
             if (!kMerge && p.l2_ahead && tc::item_pos(it + p.l2_ahead, P, C, units, H, f))
               for (int hb = 0; hb < 2; ++hb) {  // L2 prefetch of a later item (long N)
@@ -642,11 +645,19 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
       d32::prefetch_map(&tk);
       d32::prefetch_map(&tv);
       int it = 0;
+      // one unit's saved S (kMerge: the two heads' S, contiguous)
+      const uint32_t sbytes = (uint32_t)(kMerge ? 2 * 32 * 32 * 4 : 64 * 64 * 4);
+      const uint8_t* gS = static_cast<const uint8_t*>(p.saved_S);
+      if (blockIdx.x < units) tc::bulk_prefetch_l2(gS + (int64_t)unit_pos<kMerge>(blockIdx.x, H).g * (kMerge ? 4096 : 16384), sbytes);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const UnitPos up = unit_pos<kMerge>(u, H);
+        // the splitter loads the next unit's S at its first chunk: have it in L2
+        if (u + (int)gridDim.x < units)
+          tc::bulk_prefetch_l2(gS + (int64_t)unit_pos<kMerge>(u + gridDim.x, H).g * (kMerge ? 4096 : 16384), sbytes);
         for (int ps = 0; ps < 2; ++ps)
           for (int c = 0; c < C; ++c, ++it) {
             const int st = slot3(it);
+            if (COTTEN_ISSUED_GATE && it == 0) mbar_wait(&br->issued, 0);  // mask loads go first
             mbar_wait(&br->slot_free[st], par3(it) ^ 1u);
             uint8_t* X = smem + kOffRing + st * kSlot;
             mbar_expect_tx(&br->raw_full[st], 2 * kRaw);

@@ -68,3 +68,20 @@ for tag in ("fwd", "bwd"):
     for it in range(min(n, 24)):
         print(f"  it {it:2d}: {us(sp[it, 1]):6.2f} {us(sp[it, 2]):6.2f} | {us(mm[it, 1]):6.2f} {us(mm[it, 2]):6.2f} | "
               f"{us(ep[it, 3]):6.2f} {us(ep[it, 4]):6.2f}")
+
+# Start-up stamps (globaltimer, us from the first CTA entry): mask warp start, flags
+# published, producer's first TMA issued, splitter past fl_full, item 0 landed
+for tag in ("fwd", "bwd"):
+    try:
+        a = np.fromfile(f"{sys.argv[1]}/{tag}.bin", dtype=np.int64).reshape(-1, 3, K, 8)
+    except FileNotFoundError:
+        continue
+    c = a[:, 2, K - 1, 4:8].astype(np.float64)
+    t = a[:, 2, K - 2, 0:5].astype(np.float64)
+    live = (c[:, 0] > 0) & (t[:, 0] > 0)
+    if not live.any():
+        continue
+    t0 = c[live, 0].min()
+    t = (t[live] - t0) / 1e3
+    names = ("mask start", "flags published", "first TMA issued", "splitter past flags", "item 0 landed")
+    print(f"{tag} start-up (us): " + "  ".join(f"{n} {t[:, i].mean():.2f}/{t[:, i].max():.2f}" for i, n in enumerate(names)))

@@ -1,6 +1,7 @@
 """One small multi-unit fwd+bwd of a chosen kernel path, for compute-sanitizer
 (memcheck / racecheck / synccheck): python scripts/sanitize_case.py <path>
-with path in tc | d32 | rt64 | rt128 | rtbf16 | generic.  Exits non-zero on a
+with path in tc | tclong | tcf64 | tcflong | tcfmerge | tcb64 | tcbpair |
+tcblong | d32 | rt64 | rt128 | rtbf16 | generic.  Exits non-zero on a
 parity failure vs the oracle (so a sanitizer run also checks the values)."""
 import sys
 
@@ -12,13 +13,20 @@ import torch  # noqa: E402
 from paper_2602_06935_b200 import _lib, inputs, ops  # noqa: E402
 
 path = sys.argv[1]
+FP = _lib.FLAG_FP32_PIPE
 B, H, N, D, dt, flags = {
     "tc": (160, 2, 200, 32, torch.float32, 0),        # 320 units on 148 CTAs, 2 chunks/unit
     "tclong": (2, 2, 700, 32, torch.float32, 0),      # 6 chunks, flush of the running sum
-    "d32": (160, 2, 50, 32, torch.float32, 0),
-    "rt64": (20, 2, 300, 64, torch.float32, 0),
+    "tcf64": (160, 2, 300, 64, torch.float32, 0),     # fp32 d_h 64 three-part kernels, 5 chunks/unit
+    "tcflong": (2, 2, 700, 64, torch.float32, 0),     # 11 chunks, flush every 8
+    "tcfmerge": (320, 2, 50, 32, torch.float32, 0),   # head pairs merged, 320 pairs on 148 CTAs
+    "tcb64": (160, 2, 300, 64, torch.bfloat16, 0),    # bf16 d_h 64
+    "tcbpair": (160, 2, 300, 32, torch.bfloat16, 0),  # bf16 d_h 32 as paired rows
+    "tcblong": (2, 2, 1100, 64, torch.bfloat16, 0),   # 9 chunks, flush every 4
+    "d32": (160, 2, 50, 32, torch.float32, FP),
+    "rt64": (20, 2, 300, 64, torch.float32, FP),
     "rt128": (8, 2, 300, 128, torch.float32, 0),
-    "rtbf16": (20, 2, 300, 32, torch.bfloat16, 0),
+    "rtbf16": (20, 2, 301, 32, torch.bfloat16, 0),    # odd N: register-tiled
     "generic": (6, 2, 70, 24, torch.float32, 0),
 }[path]
 h = inputs.make_host(B, H, N, D, seed=1)
