@@ -728,13 +728,20 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
         Ls.append(t)
 
     def step():
+        # forward of every layer, then backward in reverse, like a training step; the
+        # device-resident cache carries Q, K, V, mask and S from each forward to its
+        # backward (the reference's AttentionCache), so the backward uploads dO only
+        caches = []
         for t in Ls:
-            _lib.check(lib.cotten_fwd_host(ctypes.byref(desc), p(t["q"]), p(t["k"]), p(t["v"]),
-                                           p(t["valid"]), 1.0, p(t["out"]), p(t["S"]), None))
-        for t in reversed(Ls):
-            _lib.check(lib.cotten_bwd_host(ctypes.byref(desc), p(t["q"]), p(t["k"]), p(t["v"]),
-                                           p(t["valid"]), 1.0, p(t["d_out"]), p(t["S"]),
-                                           p(t["dq"]), p(t["dk"]), p(t["dv"]), None, p(t["dm"])))
+            c = ctypes.c_void_p()
+            _lib.check(lib.cotten_fwd_host_cached(ctypes.byref(desc), p(t["q"]), p(t["k"]),
+                                                  p(t["v"]), p(t["valid"]), 1.0, p(t["out"]), None,
+                                                  ctypes.byref(c)))
+            caches.append(c)
+        for t, c in zip(reversed(Ls), reversed(caches)):
+            _lib.check(lib.cotten_bwd_host_cached(c, p(t["d_out"]), p(t["dq"]), p(t["dk"]),
+                                                  p(t["dv"]), None, p(t["dm"])))
+            _lib.check(lib.cotten_host_cache_free(c))
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -745,13 +752,13 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
     el = max_over_ranks(time.perf_counter() - t0, world)
     es = 2 if dname == "bf16" else 4
     tb = B * H * N * D * es
-    sb = B * H * D * D * 4
-    h2d = layers * (3 * tb + B * N) + layers * (4 * tb + B * N + sb)
-    d2h = layers * (tb + sb) + layers * (3 * tb + 8)
+    h2d = layers * (3 * tb + B * N) + layers * tb  # fwd: Q, K, V, mask; bwd: dO
+    d2h = layers * tb + layers * (3 * tb + 8)      # fwd: O; bwd: dQ, dK, dV, dm
     return {"value": global_b * args.steps / el, "unit": "seq/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
-            "path": "cotten_fwd_host + cotten_bwd_host per layer (pinned host buffers, "
-                    "host wall clock around the synchronous calls)"}
+            "path": "cotten_fwd_host_cached + cotten_bwd_host_cached per layer (the "
+                    "reference's AttentionCache kept on the device; pinned host buffers, host "
+                    "wall clock around the synchronous calls)"}
 
 
 # Core-seconds per sequence per (head * N * d_h^2) of the reference operator

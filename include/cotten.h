@@ -138,6 +138,23 @@ int cotten_fwd_bwd_host(const cotten_desc* desc, const void* q, const void* k, c
                         const uint8_t* valid, double m, const void* d_out, void* out, void* dq,
                         void* dk, void* dv, double* dm_total);
 
+/* Device-resident AttentionCache (attention.hpp:35-54) for the host entry
+ * points.  The reference's backward takes only the cache and dO
+ * (cosine_attention_backward(cache, d_out), attention.cpp:397): the cached
+ * forward keeps its staged Q, K, V, mask and state S on the device, so the
+ * backward uploads dO alone (the uncached pair uploads Q, K, V twice).
+ * Opaque and caller-owned; cotten_host_cache_free returns its device buffers
+ * to a per-device pool, so a training loop that frees each step's caches
+ * allocates nothing after its first step.  The backward may run on another
+ * host thread than the forward (same device). */
+typedef struct cotten_host_cache cotten_host_cache;
+int cotten_fwd_host_cached(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                           const uint8_t* valid, double m, void* out, void* saved_norms,
+                           cotten_host_cache** cache);
+int cotten_bwd_host_cached(const cotten_host_cache* cache, const void* d_out, void* dq, void* dk,
+                           void* dv, double* dm_unit, double* dm_total);
+int cotten_host_cache_free(cotten_host_cache* cache);
+
 /* Number of kernel launches the last device call on this thread issued. */
 int cotten_last_launch_count(void);
 

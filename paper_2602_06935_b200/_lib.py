@@ -83,6 +83,10 @@ SIGNATURES = {
                                        _vp, _vp]),
     "cotten_fwd_bwd_host": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _dbl, _vp, _vp, _vp, _vp,
                                            _vp, _vp]),
+    "cotten_fwd_host_cached": (ctypes.c_int, [_DP, _vp, _vp, _vp, _vp, _dbl, _vp, _vp,
+                                              ctypes.POINTER(_vp)]),
+    "cotten_bwd_host_cached": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "cotten_host_cache_free": (ctypes.c_int, [_vp]),
     "cotten_profile_begin": (ctypes.c_int, [_vp, ctypes.c_int]),
     "cotten_profile_end": (ctypes.c_int, []),
 }

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <type_traits>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -717,6 +718,177 @@ int cotten_bwd_host(const cotten_desc* desc, const void* q, const void* k, const
       d2h(dm_total, gdm + L.units(), sizeof(double));
     }
     COTTEN_CUDA(cudaStreamSynchronize(g_host->stream));
+  });
+}
+
+}  // extern "C"
+
+// ---- device-resident host cache -----------------------------------------------
+struct cotten_host_cache {
+  Layout L;
+  double m = 0.0;
+  int dev = 0;
+  void* q = nullptr;
+  void* k = nullptr;
+  void* v = nullptr;
+  uint8_t* mask = nullptr;
+  void* S = nullptr;
+  size_t tb = 0, mbytes = 0, sbytes = 0;
+};
+
+namespace {
+// Per-device pool of the caches' device buffers (first fit by size).
+std::mutex g_pool_mu;
+std::map<int, std::multimap<size_t, void*>> g_pool;
+void* pool_get(int dev, size_t bytes) {
+  if (bytes == 0) return nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto& fl = g_pool[dev];
+    auto it = fl.lower_bound(bytes);
+    if (it != fl.end() && it->first <= 2 * bytes) {
+      void* p = it->second;
+      fl.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  COTTEN_CUDA(cudaMalloc(&p, bytes));
+  return p;
+}
+void pool_put(int dev, void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool[dev].emplace(bytes, p);
+}
+// Capacity actually held by a pooled block is >= the request; keep the request
+// size rounded so the block returns to a bucket that serves the same shape.
+size_t pool_round(size_t b) { return (b + 4095) & ~size_t(4095); }
+}  // namespace
+
+extern "C" {
+
+int cotten_fwd_host_cached(const cotten_desc* desc, const void* q, const void* k, const void* v,
+                           const uint8_t* valid, double m, void* out, void* saved_norms,
+                           cotten_host_cache** cache) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!cache) usage("cosine_attention_fused: null cache output");
+    *cache = nullptr;
+    Layout L = resolve(desc, "cosine_attention_fused");
+    if (!q || !k || !v) usage("cosine_attention_fused: null input");
+    host_check_mask(L, valid, "cosine_attention_fused");
+    L.require_dense("cosine_attention_fused");
+    host_begin();
+    std::unique_ptr<cotten_host_cache> c(new cotten_host_cache);
+    c->L = L;
+    c->m = m;
+    COTTEN_CUDA(cudaGetDevice(&c->dev));
+    const size_t es = elem_size(L.dtype), as = acc_size(L.dtype);
+    c->tb = pool_round(L.span() * es);
+    c->mbytes = valid ? pool_round((L.B - 1) * L.msb + L.N) : 0;
+    c->sbytes = pool_round(L.units() * L.D * L.D * as);
+    auto release = [&] {
+      pool_put(c->dev, c->q, c->tb);
+      pool_put(c->dev, c->k, c->tb);
+      pool_put(c->dev, c->v, c->tb);
+      pool_put(c->dev, c->mask, c->mbytes);
+      pool_put(c->dev, c->S, c->sbytes);
+    };
+    try {
+      c->q = pool_get(c->dev, c->tb);
+      c->k = pool_get(c->dev, c->tb);
+      c->v = pool_get(c->dev, c->tb);
+      c->mask = static_cast<uint8_t*>(pool_get(c->dev, c->mbytes));
+      c->S = pool_get(c->dev, c->sbytes);
+      const size_t tb = L.span() * es;
+      const size_t nbytes = L.units() * 2 * L.N * as;
+      void* dout = out ? g_host->buf(kO, tb) : nullptr;
+      void* dN = saved_norms ? g_host->buf(kNorms, nbytes) : nullptr;
+      const Slices sl = plan_slices(L, tb);
+      for (int i = 0; i < sl.n; ++i) {  // pipelined slices, as cotten_fwd_host
+        cudaStream_t st = g_host->pipe[i % kPipe];
+        const int64_t b0 = i * sl.per, nb = std::min(sl.per, L.B - b0);
+        Layout Lc = L;
+        Lc.B = nb;
+        const size_t off = b0 * L.sb * es, len = sl.bytes(L, nb, es);
+        const size_t soff = b0 * L.H * L.D * L.D * as;
+        const size_t noff = b0 * L.H * 2 * L.N * as, nlen = nb * L.H * 2 * L.N * as;
+        pipe_h2d(at(c->q, off), at(q, off), len, st);
+        pipe_h2d(at(c->k, off), at(k, off), len, st);
+        pipe_h2d(at(c->v, off), at(v, off), len, st);
+        if (c->mask) pipe_h2d(c->mask + b0 * L.msb, valid + b0 * L.msb, (nb - 1) * L.msb + L.N, st);
+        device_fwd(Lc, at(c->q, off), at(c->k, off), at(c->v, off),
+                   c->mask ? c->mask + b0 * L.msb : nullptr, m, at(dout, off), at(c->S, soff),
+                   at(dN, noff), st);
+        pipe_d2h(at(out, off), at(dout, off), out ? len : 0, st);
+        pipe_d2h(at(saved_norms, noff), at(dN, noff), saved_norms ? nlen : 0, st);
+      }
+      pipe_sync();
+    } catch (...) {
+      release();
+      throw;
+    }
+    *cache = c.release();
+  });
+}
+
+int cotten_bwd_host_cached(const cotten_host_cache* c, const void* d_out, void* dq, void* dk,
+                           void* dv, double* dm_unit, double* dm_total) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!c) usage("cosine_attention_backward: missing cache");  // UsageError, attention.cpp:398-400
+    if (!d_out) usage("cosine_attention_backward: null input");
+    if (!dq || !dk || !dv) usage("cosine_attention_backward: null gradient output");
+    int cur = 0;
+    COTTEN_CUDA(cudaGetDevice(&cur));
+    if (cur != c->dev) usage("cosine_attention_backward: cache belongs to another device");
+    const Layout& L = c->L;
+    host_begin();
+    const size_t es = elem_size(L.dtype), as = acc_size(L.dtype);
+    const size_t tb = L.span() * es;
+    void* gdo = g_host->buf(kDO, tb);
+    void* gdq = g_host->buf(kDQ, tb);
+    void* gdk = g_host->buf(kDK, tb);
+    void* gdv = g_host->buf(kDV, tb);
+    double* gdm = static_cast<double*>(g_host->buf(kDm, (L.units() + 1) * sizeof(double)));
+    const Slices sl = plan_slices(L, tb);
+    for (int i = 0; i < sl.n; ++i) {
+      cudaStream_t st = g_host->pipe[i % kPipe];
+      const int64_t b0 = i * sl.per, nb = std::min(sl.per, L.B - b0);
+      Layout Lc = L;
+      Lc.B = nb;
+      const size_t off = b0 * L.sb * es, len = sl.bytes(L, nb, es);
+      const size_t soff = b0 * L.H * L.D * L.D * as;
+      pipe_h2d(at(gdo, off), at(d_out, off), len, st);
+      device_bwd(Lc, at(c->q, off), at(c->k, off), at(c->v, off),
+                 c->mask ? c->mask + b0 * L.msb : nullptr, c->m, at(gdo, off), at(c->S, soff),
+                 at(gdq, off), at(gdk, off), at(gdv, off), gdm + b0 * L.H, nullptr, st);
+      pipe_d2h(at(dq, off), at(gdq, off), len, st);
+      pipe_d2h(at(dk, off), at(gdk, off), len, st);
+      pipe_d2h(at(dv, off), at(gdv, off), len, st);
+      pipe_d2h(dm_unit ? dm_unit + b0 * L.H : nullptr, gdm + b0 * L.H, nb * L.H * sizeof(double), st);
+    }
+    pipe_sync();
+    if (dm_total) {  // the same partition and tree as the single-launch total (bit-identical)
+      dm_reduce_kernel<<<1, 256, 0, g_host->stream>>>(gdm, L.units(), gdm + L.units());
+      g_launches += 1;
+      COTTEN_CUDA(cudaGetLastError());
+      d2h(dm_total, gdm + L.units(), sizeof(double));
+    }
+    COTTEN_CUDA(cudaStreamSynchronize(g_host->stream));
+  });
+}
+
+int cotten_host_cache_free(cotten_host_cache* c) {
+  return guarded([&] {
+    if (!c) return;
+    pool_put(c->dev, c->q, c->tb);
+    pool_put(c->dev, c->k, c->tb);
+    pool_put(c->dev, c->v, c->tb);
+    pool_put(c->dev, c->mask, c->mbytes);
+    pool_put(c->dev, c->S, c->sbytes);
+    delete c;
   });
 }
 

@@ -1,7 +1,9 @@
 """GPU tests of the C-ABI's edge contracts: host entry points on dense layouts
 whose batch is not the outermost dimension, outputs allocated for a gapped
-(fused-projection) q, and per-stream workspaces (two streams of one host
-thread, both asking for the in-kernel dm total)."""
+(fused-projection) q, per-stream workspaces (two streams of one host thread,
+both asking for the in-kernel dm total), and the device-resident host cache
+(cotten_*_host_cached: bit-identical to the uncached pair, backward on another
+thread, pooled buffers, the missing-cache UsageError of attention.cpp:398-400)."""
 import ctypes
 
 import numpy as np
@@ -117,3 +119,87 @@ def test_two_streams_one_thread_dm_total():
         torch.cuda.synchronize()
         for t, tot in zip(sets, tots):
             assert tot.item() == t["ref"].item(), rep
+
+
+def _host_inputs(B, H, N, D, seed, dtype="f32"):
+    torch = _torch()
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    h = inputs.make_host(B, H, N, D, seed=seed)
+    t = {n: torch.from_numpy(x).to(tdt).contiguous() for n, x in h.items()}
+    t["valid"] = torch.from_numpy(inputs.left_padded_mask(B, N, seed)).contiguous()
+    return t
+
+
+@pytest.mark.parametrize("D,dtype,N", [(32, "f32", 200), (64, "f32", 300), (32, "bf16", 256),
+                                       (32, "f32", 50)])
+def test_cached_host_pair_equals_uncached_host_pair(D, dtype, N):
+    """cotten_fwd_host_cached / cotten_bwd_host_cached (the AttentionCache kept on
+    the device) give bit-identical outputs to cotten_fwd_host / cotten_bwd_host."""
+    torch = _torch()
+    lib = _lib.load()
+    B, H = 37, 2
+    t = _host_inputs(B, H, N, D, seed=D + N, dtype=dtype)
+    desc = _lib.make_desc(B, H, N, D, dtype, 1e-6)
+    z = lambda: torch.empty_like(t["q"])  # noqa: E731
+    o1, dq1, dk1, dv1 = z(), z(), z(), z()
+    S = torch.empty(B * H, D, D)
+    dm1 = torch.zeros(1, dtype=torch.float64)
+    _lib.check(lib.cotten_fwd_host(ctypes.byref(desc), _ptr(t["q"]), _ptr(t["k"]), _ptr(t["v"]),
+                                   _ptr(t["valid"]), 0.75, _ptr(o1), _ptr(S), None))
+    _lib.check(lib.cotten_bwd_host(ctypes.byref(desc), _ptr(t["q"]), _ptr(t["k"]), _ptr(t["v"]),
+                                   _ptr(t["valid"]), 0.75, _ptr(t["d_out"]), _ptr(S), _ptr(dq1),
+                                   _ptr(dk1), _ptr(dv1), None, _ptr(dm1)))
+    o2, dq2, dk2, dv2 = z(), z(), z(), z()
+    dm2 = torch.zeros(1, dtype=torch.float64)
+    dmu = torch.zeros(B * H, dtype=torch.float64)
+    c = ctypes.c_void_p()
+    _lib.check(lib.cotten_fwd_host_cached(ctypes.byref(desc), _ptr(t["q"]), _ptr(t["k"]),
+                                          _ptr(t["v"]), _ptr(t["valid"]), 0.75, _ptr(o2), None,
+                                          ctypes.byref(c)))
+    assert c.value
+    _lib.check(lib.cotten_bwd_host_cached(c, _ptr(t["d_out"]), _ptr(dq2), _ptr(dk2), _ptr(dv2),
+                                          _ptr(dmu), _ptr(dm2)))
+    _lib.check(lib.cotten_host_cache_free(c))
+    for a, b in ((o1, o2), (dq1, dq2), (dk1, dk2), (dv1, dv2), (dm1, dm2)):
+        assert torch.equal(a, b)
+    assert float(dm2) == pytest.approx(float(dmu.sum()), rel=1e-12, abs=1e-12)
+
+
+def test_cached_backward_on_another_thread_and_pool_reuse():
+    import threading
+    torch = _torch()
+    lib = _lib.load()
+    B, H, N, D = 20, 2, 200, 32
+    t = _host_inputs(B, H, N, D, seed=3)
+    desc = _lib.make_desc(B, H, N, D, "f32", 1e-6)
+    outs = []
+    for rep in range(3):  # freed caches' device buffers are reused by the next forward
+        c = ctypes.c_void_p()
+        o = torch.empty_like(t["q"])
+        _lib.check(lib.cotten_fwd_host_cached(ctypes.byref(desc), _ptr(t["q"]), _ptr(t["k"]),
+                                              _ptr(t["v"]), _ptr(t["valid"]), 1.0, _ptr(o), None,
+                                              ctypes.byref(c)))
+        g = [torch.empty_like(t["q"]) for _ in range(3)]
+        rc = []
+        th = threading.Thread(target=lambda: rc.append(lib.cotten_bwd_host_cached(
+            c, _ptr(t["d_out"]), _ptr(g[0]), _ptr(g[1]), _ptr(g[2]), None, None)))
+        th.start()
+        th.join()
+        assert rc == [0]
+        _lib.check(lib.cotten_host_cache_free(c))
+        outs.append((o, *g))
+    for a, b in zip(outs[0], outs[2]):
+        assert torch.equal(a, b)
+    ref = oracle.batched_f32(t["q"].numpy(), t["k"].numpy(), t["v"].numpy(), t["d_out"].numpy(),
+                             t["valid"].numpy(), 1.0, 1e-6)
+    for got, want in zip(outs[0], ref[:4]):
+        g = got.double().numpy().reshape(B * H, -1)
+        w = want.reshape(B * H, -1)
+        assert float((np.abs(g - w).max(1) / np.abs(w).max(1)).max()) <= 1e-5
+
+
+def test_cached_backward_without_cache_is_usage_error():
+    lib = _lib.load()
+    rc = lib.cotten_bwd_host_cached(None, None, None, None, None, None, None)
+    assert rc == _lib.COTTEN_ERR_USAGE
+    assert b"missing cache" in lib.cotten_last_error()
