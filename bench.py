@@ -734,7 +734,7 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
     # The reference calls the op from parallel_chunks workers (encoder.cpp:295,345); the
     # host entry points are thread-safe with per-thread streams, so W host threads each
     # run the step on a contiguous slice of the batch and their PCIe transfers overlap.
-    W = max(1, min(B, int(os.environ.get("COTTEN_E2E_THREADS", "4"))))
+    W = max(1, min(B, int(os.environ.get("COTTEN_E2E_THREADS", "2"))))
     es = 2 if dname == "bf16" else 4
     per = (B + W - 1) // W
     slices = [(b0, min(B, b0 + per)) for b0 in range(0, B, per)]
