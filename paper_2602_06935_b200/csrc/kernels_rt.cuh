@@ -39,20 +39,28 @@
 namespace cotten {
 namespace rt {
 
-constexpr int kThreads = 256;
+#ifndef COTTEN_RT128_THREADS
+#define COTTEN_RT128_THREADS 256
+#endif
 
 template <int D>
 struct Cfg {
+  // threads per CTA: d_h 128 runs one CTA per SM (its state alone is 64-128 KB,
+  // ncu: 12.5 % warps active, short-scoreboard stalls first); 512 threads
+  // (COTTEN_RT128_THREADS=512: CB 32, RC 4) measured no faster — the
+  // shared-memory port (L1/TEX 69-79 %) bounds it, not latency
+  // (profiles/r02aa_rt512) — so 256 stays
+  static constexpr int NT = D >= 128 ? COTTEN_RT128_THREADS : 256;
   // thread tid = (row index) * CB + cb: cb picks the 4-column groups
   // cb + CB g of a row (state and outputs alike)
-  static constexpr int CB = D / 4 < 16 ? D / 4 : 16;  // column-group threads (8 / 16 / 16)
-  static constexpr int RB = kThreads / CB;             // distinct row indices (32 / 16 / 16)
-  static constexpr int RC = D / CB;                    // columns per thread (4 / 4 / 8)
-  static constexpr int RA = D * D / (kThreads * RC);   // state rows per thread (1 / 4 / 8)
-  static constexpr int RR = 16 / RC;                   // output rows per thread (4 / 4 / 2)
-  static constexpr int TR = RB * RR;                   // tile rows (128 / 64 / 32)
-  static constexpr int F4 = D / 4;              // 4-element groups per row
-  static constexpr int LD = TR * F4 / kThreads; // 4-element loads per thread per tile
+  static constexpr int CB = (D >= 128 && NT == 512) ? 32 : (D / 4 < 16 ? D / 4 : 16);  // 8 / 16 / 32
+  static constexpr int RB = NT / CB;             // distinct row indices (32 / 16 / 16)
+  static constexpr int RC = D / CB;              // columns per thread (4 / 4 / 4)
+  static constexpr int RA = D * D / (NT * RC);   // state rows per thread (1 / 4 / 8)
+  static constexpr int RR = (D >= 128 && NT == 512) ? 2 : 16 / RC;  // output rows per thread (4 / 4 / 2)
+  static constexpr int TR = RB * RR;             // tile rows (128 / 64 / 32)
+  static constexpr int F4 = D / 4;               // 4-element groups per row
+  static constexpr int LD = TR * F4 / NT;        // 4-element loads per thread per tile
   static constexpr int kFlushTiles = 512 / TR;  // running-sum flush period (512 rows)
   // tile row stride: +16 B so rows rb and rb + 1 (read together by a warp in
   // the row outputs) fall in different banks
@@ -60,7 +68,8 @@ struct Cfg {
   // two tile buffers (double-buffered: tile i+1's loads are in flight while
   // tile i is computed) of two tensors each, the state(s), 1/norm per buffer
   static constexpr size_t fwd_smem = sizeof(float) * (4 * TR * LDT + D * D + 2 * TR);
-  static constexpr size_t bwd_smem = sizeof(float) * (4 * TR * LDT + 2 * D * D + 2 * TR) + 8 * sizeof(double);
+  static constexpr size_t bwd_smem =
+      sizeof(float) * (4 * TR * LDT + 2 * D * D + 2 * TR) + (NT / 32) * sizeof(double);
 };
 
 __device__ __forceinline__ float4 ld4(const float* p) {
@@ -93,7 +102,7 @@ __device__ __forceinline__ void fetch_tile(float4 (&reg)[Cfg<D>::LD], const T* X
   using C = Cfg<D>;
 #pragma unroll
   for (int k = 0; k < C::LD; ++k) {
-    const int f = threadIdx.x + kThreads * k;
+    const int f = threadIdx.x + C::NT * k;
     const int64_t row = t0 + f / C::F4;
     reg[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (row < N) reg[k] = ld4(X + base + row * sn + 4 * (f % C::F4));
@@ -110,7 +119,7 @@ __device__ __forceinline__ void put_tile(float* sm, float* rinv, const float4 (&
   using C = Cfg<D>;
 #pragma unroll
   for (int k = 0; k < C::LD; ++k) {
-    const int f = threadIdx.x + kThreads * k;
+    const int f = threadIdx.x + C::NT * k;
     const int r = f / C::F4, c4 = f % C::F4;
     const int64_t row = t0 + r;
     float4 v = reg[k];
@@ -250,7 +259,7 @@ __device__ __forceinline__ void store_row(T* dst, const float (&o)[Cfg<D>::RC], 
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
+__global__ void __launch_bounds__(Cfg<D>::NT) cos_fwd_rt(const OpParams p) {
   const KernelStamp stamp_(p);
   using C = Cfg<D>;
   extern __shared__ __align__(16) float sm[];
@@ -273,7 +282,7 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
   const float scale = (float)exp(-op_m(p) * log((double)true_n));  // :303-304, in fp64
   const float eps = (float)p.eps;
   const int tid = threadIdx.x, ab = tid / C::CB, cb = tid % C::CB;
-  for (int e = tid; e < D * D; e += kThreads) Ssm[e] = 0.f;
+  for (int e = tid; e < D * D; e += C::NT) Ssm[e] = 0.f;
 
   float acc[C::RA][C::RC];
 #pragma unroll
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
   __syncthreads();
   if (p.saved_S) {
     float* dst = static_cast<float*>(p.saved_S) + unit * (int64_t)D * D;
-    for (int e = tid; e < D * D / 4; e += kThreads)
+    for (int e = tid; e < D * D / 4; e += C::NT)
       reinterpret_cast<float4*>(dst)[e] = reinterpret_cast<const float4*>(Ssm)[e];
   }
   if (p.out == nullptr && norms == nullptr) return;
@@ -334,7 +343,7 @@ __global__ void __launch_bounds__(kThreads) cos_fwd_rt(const OpParams p) {
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
+__global__ void __launch_bounds__(Cfg<D>::NT) cos_bwd_rt(const OpParams p) {
   const KernelStamp stamp_(p);
   using C = Cfg<D>;
   extern __shared__ __align__(16) float sm[];
@@ -368,7 +377,7 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
 
   // S^T into Bt (Bt[c][a] = S[a][c], conflict-free smem writes), G = 0
   const float* gS = static_cast<const float*>(p.saved_S) + unit * (int64_t)D * D;
-  for (int e = tid; e < D * D; e += kThreads) {
+  for (int e = tid; e < D * D; e += C::NT) {
     const int c = e / D, a = e - c * D;
     Bt[e] = __ldg(gS + a * D + c);
     Bn[e] = 0.f;
@@ -428,7 +437,7 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
   // dm = -ln(n) s <G, S> (:408): fixed-order (thread, warp tree, warps in order)
   {
     double part = 0.0;
-    for (int e = tid; e < D * D; e += kThreads) {
+    for (int e = tid; e < D * D; e += C::NT) {
       const int a = e / D, c = e - a * D;
       part += (double)(Bn[e] * Bt[c * D + a]);
     }
@@ -438,17 +447,17 @@ __global__ void __launch_bounds__(kThreads) cos_bwd_rt(const OpParams p) {
     __syncthreads();
     if (tid == 0 && p.dm_unit) {
       double dot = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) dot += red[w];
+      for (int w = 0; w < C::NT / 32; ++w) dot += red[w];
       p.dm_unit[unit] = -log_n * (double)scale * dot;
     }
   }
   // dA = s G (:412-413): dA^T into Bt (B of dK~ = V dA^T), dA in place in Bn (B of dV = K~ dA)
-  for (int e = tid; e < D * D; e += kThreads) {
+  for (int e = tid; e < D * D; e += C::NT) {
     const int c = e / D, a = e - c * D;
     Bt[e] = scale * Bn[a * D + c];
   }
   __syncthreads();
-  for (int e = tid; e < D * D; e += kThreads) Bn[e] *= scale;
+  for (int e = tid; e < D * D; e += C::NT) Bn[e] *= scale;
 
   // Phase B: dK (valid rows), dV (valid rows); padded rows exact zeros (:430-439)
   nt = 0;
@@ -521,23 +530,23 @@ inline bool rt_supported(const OpParams& p, bool bwd) {
 
 template <typename T>
 inline void launch_rt_fwd(const OpParams& p, cudaStream_t st) {
-  auto go = [&](auto kern, size_t smem) {
+  auto go = [&](auto kern, size_t smem, int nt) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)(p.B * p.H), rt::kThreads, smem, st>>>(p);
+    kern<<<(unsigned)(p.B * p.H), nt, smem, st>>>(p);
   };
-  if (p.D == 32) go(rt::cos_fwd_rt<T, 32>, rt::Cfg<32>::fwd_smem);
-  else if (p.D == 64) go(rt::cos_fwd_rt<T, 64>, rt::Cfg<64>::fwd_smem);
-  else go(rt::cos_fwd_rt<T, 128>, rt::Cfg<128>::fwd_smem);
+  if (p.D == 32) go(rt::cos_fwd_rt<T, 32>, rt::Cfg<32>::fwd_smem, rt::Cfg<32>::NT);
+  else if (p.D == 64) go(rt::cos_fwd_rt<T, 64>, rt::Cfg<64>::fwd_smem, rt::Cfg<64>::NT);
+  else go(rt::cos_fwd_rt<T, 128>, rt::Cfg<128>::fwd_smem, rt::Cfg<128>::NT);
 }
 template <typename T>
 inline void launch_rt_bwd(const OpParams& p, cudaStream_t st) {
-  auto go = [&](auto kern, size_t smem) {
+  auto go = [&](auto kern, size_t smem, int nt) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)(p.B * p.H), rt::kThreads, smem, st>>>(p);
+    kern<<<(unsigned)(p.B * p.H), nt, smem, st>>>(p);
   };
-  if (p.D == 32) go(rt::cos_bwd_rt<T, 32>, rt::Cfg<32>::bwd_smem);
-  else if (p.D == 64) go(rt::cos_bwd_rt<T, 64>, rt::Cfg<64>::bwd_smem);
-  else go(rt::cos_bwd_rt<T, 128>, rt::Cfg<128>::bwd_smem);
+  if (p.D == 32) go(rt::cos_bwd_rt<T, 32>, rt::Cfg<32>::bwd_smem, rt::Cfg<32>::NT);
+  else if (p.D == 64) go(rt::cos_bwd_rt<T, 64>, rt::Cfg<64>::bwd_smem, rt::Cfg<64>::NT);
+  else go(rt::cos_bwd_rt<T, 128>, rt::Cfg<128>::bwd_smem, rt::Cfg<128>::NT);
 }
 
 }  // namespace cotten
