@@ -1,12 +1,13 @@
 # Round-2 measurement record: GPU suite, smoke, default bench + reference arm, every workload line,
 # the config #5 sweep, the ncu launch list of the default bench command.
+rm -rf gpurun_out/final gpurun_out/sweep
 mkdir -p gpurun_out/final
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/final/gpu.csv 2>&1
 timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/final/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/final/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/final/smoke.log
 timeout 900 python bench.py > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/final/bench_ref.json 2>> gpurun_out/final/bench.err
-for w in ml20m beauty long4k long16k long4k_d64 long4k_d128 long4k_bf16 long4k_d64_bf16 long4k_d128_bf16; do
+for w in ml1m_d64 ml20m beauty long4k long16k long4k_d64 long4k_d128 long4k_bf16 long4k_d64_bf16 long4k_d128_bf16; do
   timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-steady --no-encoder > gpurun_out/final/bench_$w.json 2>> gpurun_out/final/bench.err
 done
 mkdir -p gpurun_out/sweep
