@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <type_traits>
+#include <condition_variable>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -467,6 +468,46 @@ struct HostCtx {
 };
 thread_local std::map<int, HostCtx> g_hosts;
 thread_local HostCtx* g_host = nullptr;
+// At most COTTEN_HOST_MAX_CONCURRENT (default 4) host-entry calls stage and run
+// at once per process; further callers queue.  The host path is PCIe-bound and
+// 2-4 concurrent callers already keep both copy directions busy, while the
+// reference calls the op from cfg.threads parallel_chunks workers: at 16 host
+// threads the gate held ML-1M e2e at 48-49 k seq/s over five windows, against
+// 4-49 k without it (profiles/r02ac_host_threads).
+class HostGate {
+ public:
+  void acquire() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return busy_ < limit(); });
+    ++busy_;
+  }
+  void release() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      --busy_;
+    }
+    cv_.notify_one();
+  }
+
+ private:
+  static int limit() {
+    static const int v = [] {
+      const char* e = std::getenv("COTTEN_HOST_MAX_CONCURRENT");
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    return v;
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  int busy_ = 0;
+};
+HostGate g_gate;
+struct HostSlot {
+  HostSlot() { g_gate.acquire(); }
+  ~HostSlot() { g_gate.release(); }
+  HostSlot(const HostSlot&) = delete;
+  HostSlot& operator=(const HostSlot&) = delete;
+};
 // Select (creating on first use) the calling thread's context on the current device.
 void host_begin() {
   int cur = 0;
@@ -625,6 +666,7 @@ int cotten_fwd_host(const cotten_desc* desc, const void* q, const void* k, const
     if (!q || !k || !v) usage("cosine_attention_fused: null input");
     host_check_mask(L, valid, "cosine_attention_fused");
     L.require_dense("cosine_attention_fused");
+    const HostSlot slot_;  // concurrency gate, held to the end of the call
     host_begin();
     const size_t tb = L.span() * elem_size(L.dtype);
     const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
@@ -670,6 +712,7 @@ int cotten_bwd_host(const cotten_desc* desc, const void* q, const void* k, const
     if (!dq || !dk || !dv) usage("cosine_attention_backward: null gradient output");
     host_check_mask(L, valid, "cosine_attention_backward");
     L.require_dense("cosine_attention_backward");
+    const HostSlot slot_;  // concurrency gate, held to the end of the call
     host_begin();
     const size_t tb = L.span() * elem_size(L.dtype);
     const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);
@@ -779,6 +822,7 @@ int cotten_fwd_host_cached(const cotten_desc* desc, const void* q, const void* k
     if (!q || !k || !v) usage("cosine_attention_fused: null input");
     host_check_mask(L, valid, "cosine_attention_fused");
     L.require_dense("cosine_attention_fused");
+    const HostSlot slot_;  // concurrency gate, held to the end of the call
     host_begin();
     std::unique_ptr<cotten_host_cache> c(new cotten_host_cache);
     c->L = L;
@@ -844,6 +888,7 @@ int cotten_bwd_host_cached(const cotten_host_cache* c, const void* d_out, void* 
     COTTEN_CUDA(cudaGetDevice(&cur));
     if (cur != c->dev) usage("cosine_attention_backward: cache belongs to another device");
     const Layout& L = c->L;
+    const HostSlot slot_;  // concurrency gate, held to the end of the call
     host_begin();
     const size_t es = elem_size(L.dtype), as = acc_size(L.dtype);
     const size_t tb = L.span() * es;
@@ -902,6 +947,7 @@ int cotten_fwd_bwd_host(const cotten_desc* desc, const void* q, const void* k, c
     if (!out || !dq || !dk || !dv) usage("cosine_attention_fused: null output");
     host_check_mask(L, valid, "cosine_attention_fused");
     L.require_dense("cosine_attention_fused");
+    const HostSlot slot_;  // concurrency gate, held to the end of the call
     host_begin();
     const size_t tb = L.span() * elem_size(L.dtype);
     const size_t sbytes = L.units() * L.D * L.D * acc_size(L.dtype);

@@ -198,6 +198,52 @@ def test_cached_backward_on_another_thread_and_pool_reuse():
         assert float((np.abs(g - w).max(1) / np.abs(w).max(1)).max()) <= 1e-5
 
 
+def test_many_host_threads_through_the_gate():
+    """12 threads (more than the default 4 concurrent host calls the gate
+    admits) each run cached fwd + bwd on their own batch slice, 3 times; every
+    slice equals the same call made alone, and nothing deadlocks."""
+    import threading
+    torch = _torch()
+    lib = _lib.load()
+    B, H, N, D, W = 48, 2, 200, 32, 12
+    t = _host_inputs(B, H, N, D, seed=9)
+    per = B // W
+    es = 4
+
+    def call(b0, outs):
+        dsc = _lib.make_desc(per, H, N, D, "f32", 1e-6)
+        off = b0 * H * N * D * es
+        q = lambda x: ctypes.c_void_p(x.data_ptr() + off)  # noqa: E731
+        c = ctypes.c_void_p()
+        rc = lib.cotten_fwd_host_cached(ctypes.byref(dsc), q(t["q"]), q(t["k"]), q(t["v"]),
+                                        ctypes.c_void_p(t["valid"].data_ptr() + b0 * N), 1.0,
+                                        q(outs[0]), None, ctypes.byref(c))
+        if rc == 0:
+            rc = lib.cotten_bwd_host_cached(c, q(t["d_out"]), q(outs[1]), q(outs[2]), q(outs[3]),
+                                            None, None)
+            lib.cotten_host_cache_free(c)
+        return rc
+
+    alone = [torch.empty_like(t["q"]) for _ in range(4)]
+    for w in range(W):
+        assert call(w * per, alone) == 0
+    for _ in range(3):
+        got = [torch.full_like(t["q"], float("nan")) for _ in range(4)]
+        rcs = [None] * W
+
+        def worker(w):
+            rcs[w] = call(w * per, got)
+        ths = [threading.Thread(target=worker, args=(w,)) for w in range(W)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join(timeout=120)
+        assert not any(th.is_alive() for th in ths)
+        assert rcs == [0] * W
+        for a, b in zip(alone, got):
+            assert torch.equal(a, b)
+
+
 def test_cached_backward_without_cache_is_usage_error():
     lib = _lib.load()
     rc = lib.cotten_bwd_host_cached(None, None, None, None, None, None, None)
