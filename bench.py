@@ -131,6 +131,8 @@ def pipe_flops(B, H, N, D):
 def kernel_path(path, N, D, dname="f32", H=2):
     """The kernels the library picks for this shape (cotten_capi.cu launch_*_t)."""
     tcb = path == "tcgen05" and not os.environ.get("COTTEN_NO_TCB")
+    if dname == "bf16" and D == 128 and path == "tcgen05" and not os.environ.get("COTTEN_NO_TCH"):
+        return "tcgen05 kind::f16 bf16x3, 64-row chunks (kernels_tch.cuh)"
     if dname == "bf16" and D == 64 and tcb:
         return "tcgen05 kind::f16 bf16x3 (kernels_tcb.cuh)"
     if dname == "bf16" and D == 32 and tcb and N % 2 == 0 and not os.environ.get("COTTEN_NO_TCB_PAIR"):

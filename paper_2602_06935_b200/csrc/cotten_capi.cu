@@ -24,6 +24,7 @@
 #include "kernels_tc.cuh"
 #include "kernels_tcb.cuh"
 #include "kernels_tcf.cuh"
+#include "kernels_tch.cuh"
 
 namespace cotten {
 namespace {
@@ -231,6 +232,11 @@ void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fp32 d_h=64 tensor-core forward launch failed"};
     g_launches += n;
+  } else if (tensor && tch_fwd_supported<T>(p)) {
+    const int n = launch_tch_fwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: bf16 d_h=128 tensor-core forward launch failed"};
+    g_launches += n;
   } else if (tensor && tcb_fwd_supported<T>(p)) {
     const int n = launch_tcb_fwd(p, st);
     COTTEN_CUDA(cudaGetLastError());
@@ -268,6 +274,11 @@ void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
     const int n = launch_tcf_bwd(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fp32 d_h=64 tensor-core backward launch failed"};
+    g_launches += n;
+  } else if (tensor && tch_bwd_supported<T>(p)) {
+    const int n = launch_tch_bwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: bf16 d_h=128 tensor-core backward launch failed"};
     g_launches += n;
   } else if (tensor && tcb_bwd_supported<T>(p)) {
     const int n = launch_tcb_bwd(p, st);
@@ -371,7 +382,8 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
   const bool tc_path = tensor && ((L.dtype == COTTEN_F32 && (tc_bwd_supported<float>(p) ||
                                                               tcf_bwd_supported<float>(p))) ||
-                                  (L.dtype == COTTEN_BF16 && tcb_bwd_supported<__nv_bfloat16>(p)));
+                                  (L.dtype == COTTEN_BF16 && (tcb_bwd_supported<__nv_bfloat16>(p) ||
+                                                               tch_bwd_supported<__nv_bfloat16>(p))));
   if (dm_total && tc_path) {  // the tcgen05 kernel's last CTA writes the total (no extra launch)
     p.dm_total = dm_total;
     p.grid_done = static_cast<unsigned*>(scratch_get(st, kScrCounter, sizeof(unsigned), true));
