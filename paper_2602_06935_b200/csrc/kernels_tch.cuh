@@ -25,7 +25,11 @@
 //    after the last MMA reading dA has completed (ops_free).
 //  * TMEM: [0, 128) S / G accumulator, [128, 256) running sum, two 128-column
 //    output buffers [256, 384) and [384, 512) taken in turn by the row-output
-//    jobs (O; dQ~; dV then dK~), each released by the epiloguer (out_free).
+//    jobs (O; dQ~), each released by the epiloguer (out_free).  The backward's
+//    pass 2 (dV and dK~ per item) also borrows the accumulator and running-sum
+//    columns, idle until the next unit's G: its items alternate between the
+//    buffer pairs (out 0, out 1) and (acc, run), so the MMAs of one item run
+//    while the epiloguer drains the previous one.
 // Shared memory 213 KB; 512 threads: 0-7 splitter (four threads per row, 32
 // columns each, granule order rotated for threads 2-3 so that an 8-lane
 // LDS.128 phase covers all 8 bank groups), 8-11 epiloguer, 12 TMA producer,
@@ -106,7 +110,7 @@ __device__ __forceinline__ uint32_t par3(int it) { return (uint32_t)(it / kRing)
 
 struct Bars {
   uint64_t raw_full[kRing], slot_free[kRing], split_full[kRing], mma_done[kRing], staged[kRing];
-  uint64_t out_free[2];
+  uint64_t out_free[4];  // out 0, out 1, acc, run as output buffers
   uint64_t op_ready, acc_free, red_done, ops_free;
   uint64_t fl_full[2], fl_empty[2];
   uint64_t issued;
@@ -167,8 +171,8 @@ __device__ __forceinline__ uint32_t setup(uint8_t* smem, Bars* br, uint32_t* tsl
       mbar_init(&br->mma_done[i], 1);
       mbar_init(&br->staged[i], kEpiWarps);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&br->out_free[i], kEpiWarps);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&br->out_free[i], kEpiWarps);
       mbar_init(&br->fl_full[i], 1);
       mbar_init(&br->fl_empty[i], kSplitWarps + kEpiWarps);
     }
@@ -218,6 +222,13 @@ __device__ __forceinline__ void arrive_staged(Bars* br, int b, int lane) {
   tc_fence_before();
   __syncwarp();
   if (lane == 0) mbar_arrive(&br->staged[b]);
+}
+// TMEM column of output buffer b (0, 1: the output columns; 2, 3: acc, run)
+__device__ __forceinline__ uint32_t out_col(int b) { return b < 2 ? kOut0 + kOutCols * b : (b == 2 ? kAcc : kRun); }
+// MMA side: wait until buffer b's previous use is drained (use parities in `par`)
+__device__ __forceinline__ void take_out(Bars* br, uint32_t& par, int b) {
+  mbar_wait(&br->out_free[b], ((par >> b) & 1u) ^ 1u);
+  par ^= 1u << b;
 }
 __device__ __forceinline__ void release_out(Bars* br, int b, int lane) {
   tc_fence_before();
@@ -555,7 +566,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tch_kernel(
       }
     }
   } else if (warp == kWarpMma) {
-    int it = 0, j = 0, nflush = 0, ob = 0;
+    int it = 0, j = 0, nflush = 0, n1 = 0, n2 = 0;
+    uint32_t par = 0;
     const uint32_t base = smem_u32(smem);
     const uint32_t opH = base + kOffOps, opL = opH + kStateTile;  // S, then dA
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
@@ -565,6 +577,9 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tch_kernel(
           mbar_wait(&br->split_full[st], par3(it));
           if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
           if (ps == 0 && c > 0 && c % kFlush == 0) mbar_wait(&br->acc_free, (nflush++) & 1);
+          // a new G overwrites the accumulator columns: the last pass-2 item that
+          // borrowed them must be drained
+          if (ps == 0 && c == 0) mbar_wait(&br->out_free[2], ((par >> 2) & 1u) ^ 1u);
           tc_fence_after();
           const uint32_t X = base + kOffRing + st * kSlot, Y = X + kTile, Z = X + 2 * kTile;
           if (ps == 0) {
@@ -574,32 +589,31 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tch_kernel(
               issue_red(tmem + kAcc, X, Y, ks, false);
             }
             __syncwarp();
-            mbar_wait(&br->out_free[ob & 1], ((ob >> 1) & 1) ^ 1u);
+            const int b = n1++ & 1;
+            take_out(br, par, b);
             tc_fence_after();
             if (elect_one()) {
               // dQ~ (unscaled) = dO S^T (:410-411): A = dO (K-major), B row n = S row n
-              issue_rowout<false>(tmem + kOut0 + kOutCols * (ob & 1), Y, opH, opL);
+              issue_rowout<false>(tmem + out_col(b), Y, opH, opL);
               // G complete, and every MMA that reads this unit's S
               if (c == C - 1) mma_commit(&br->red_done);
               mma_commit(&br->mma_done[st]);
             }
             __syncwarp();
-            ++ob;
           } else {
-            mbar_wait(&br->out_free[ob & 1], ((ob >> 1) & 1) ^ 1u);
+            const int pr = (n2++ & 1) * 2;  // buffer pair (0, 1) or (2, 3)
+            take_out(br, par, pr);
             tc_fence_after();
-            if (elect_one()) issue_rowout3<true>(tmem + kOut0 + kOutCols * (ob & 1), Z, X, opH, opL);  // dV = K~ dA (:416)
+            if (elect_one()) issue_rowout3<true>(tmem + out_col(pr), Z, X, opH, opL);  // dV = K~ dA (:416)
             __syncwarp();
-            ++ob;
-            mbar_wait(&br->out_free[ob & 1], ((ob >> 1) & 1) ^ 1u);
+            take_out(br, par, pr + 1);
             tc_fence_after();
             if (elect_one()) {
-              issue_rowout<false>(tmem + kOut0 + kOutCols * (ob & 1), Y, opH, opL);  // dK~ = V dA^T (:415)
+              issue_rowout<false>(tmem + out_col(pr + 1), Y, opH, opL);  // dK~ = V dA^T (:415)
               mma_commit(&br->mma_done[st]);
               if (c == C - 1) mma_commit(&br->ops_free);  // every MMA reading this unit's dA
             }
             __syncwarp();
-            ++ob;
           }
         }
     }
@@ -637,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tch_kernel(
     const float* gS_all = static_cast<const float*>(p.saved_S);
     const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
     const float qnan = __int_as_float(0x7fc00000);
-    int it = 0, j = 0, ob = 0;
+    int it = 0, j = 0, n1 = 0, n2 = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int sl = j & 1;
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(smem + kOffFlags + sl * (kMaxN / 8));
@@ -730,9 +744,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tch_kernel(
           const int row = 16 * wq + (lane & 15), h = lane >> 4;
           const int r = c * kRows + row;
           const float iv = inv_st[row];
-          // g = dQ~ (pass 1) or dK~ (pass 2, the item's second buffer); pr = g . x~
-          const int bg = ps == 0 ? (ob & 1) : ((ob + 1) & 1);
-          const uint32_t Dg = tmem + kOut0 + kOutCols * bg + lane_base;
+          // g = dQ~ (pass 1) or dK~ (pass 2, the second buffer of the item's pair); pr = g . x~
+          const int bv = (n2 & 1) * 2;  // pass 2: dV in bv, dK~ in bv + 1
+          const int bg = ps == 0 ? (n1 & 1) : bv + 1;
+          const uint32_t Dg = tmem + out_col(bg) + lane_base;
           float pr = 0.f;
 #pragma unroll 1
           for (int hh = 0; hh < 2; ++hh) {
@@ -754,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tch_kernel(
               store_half(Z + hh * kHalf, row, h, g);
             }
             release_out(br, bg, lane);
-            ++ob;
+            ++n1;
           } else {
             const bool f = r < N && tc::flag_at(fl, r);
             const bool nan_out = uc.tn == 0;
@@ -770,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tch_kernel(
             }
             release_out(br, bg, lane);
             // dV_i = v_i ? (K~ dA)_i : 0 (:416, :439), staged in Z (K~ is done)
-            const uint32_t Dv = tmem + kOut0 + kOutCols * (ob & 1) + lane_base;
+            const uint32_t Dv = tmem + out_col(bv) + lane_base;
 #pragma unroll 1
             for (int hh = 0; hh < 2; ++hh) {
               float g[32];
@@ -779,8 +794,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tch_kernel(
               for (int e = 0; e < 32; ++e) g[e] = nan_out ? qnan : (f ? g[e] : 0.f);
               store_half(Z + hh * kHalf, row, h, g);
             }
-            release_out(br, ob & 1, lane);
-            ob += 2;
+            release_out(br, bv, lane);
+            ++n2;
           }
           arrive_staged(br, st, lane);
         }
