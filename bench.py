@@ -139,6 +139,8 @@ def kernel_path(path, N, D, dname="f32", H=2):
         return "tcgen05 kind::f16 bf16x3, paired rows (kernels_tcb.cuh)"
     if dname == "bf16" and D == 32:
         return "fp32-rt register-tiled FP32 pipe (kernels_rt.cuh)"
+    if dname == "f32" and D == 128 and path == "tcgen05" and not os.environ.get("COTTEN_NO_TCG"):
+        return "tcgen05 kind::f16, fp32 as three bf16 parts, 32-row items (kernels_tcg.cuh)"
     if dname == "f32" and D == 64 and tcb and not os.environ.get("COTTEN_NO_TCF"):
         return "tcgen05 kind::f16, fp32 as three bf16 parts (kernels_tcf.cuh)"
     if D == 32 and path == "tcgen05" and N > 64:

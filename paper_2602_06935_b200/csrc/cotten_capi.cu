@@ -25,6 +25,7 @@
 #include "kernels_tcb.cuh"
 #include "kernels_tcf.cuh"
 #include "kernels_tch.cuh"
+#include "kernels_tcg.cuh"
 
 namespace cotten {
 namespace {
@@ -227,7 +228,12 @@ template <typename T>
 void launch_fwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
-  if (tensor && tcf_fwd_supported<T>(p)) {
+  if (tensor && tcg_fwd_supported<T>(p)) {
+    const int n = launch_tcg_fwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fp32 d_h=128 tensor-core forward launch failed"};
+    g_launches += n;
+  } else if (tensor && tcf_fwd_supported<T>(p)) {
     const int n = launch_tcf_fwd(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fp32 d_h=64 tensor-core forward launch failed"};
@@ -270,7 +276,12 @@ template <typename T>
 void launch_bwd_t(const Layout& L, OpParams p, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
-  if (tensor && tcf_bwd_supported<T>(p)) {
+  if (tensor && tcg_bwd_supported<T>(p)) {
+    const int n = launch_tcg_bwd(p, st);
+    COTTEN_CUDA(cudaGetLastError());
+    if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fp32 d_h=128 tensor-core backward launch failed"};
+    g_launches += n;
+  } else if (tensor && tcf_bwd_supported<T>(p)) {
     const int n = launch_tcf_bwd(p, st);
     COTTEN_CUDA(cudaGetLastError());
     if (n < 0) throw Error{COTTEN_ERR_INTERNAL, "cotten: fp32 d_h=64 tensor-core backward launch failed"};
@@ -381,7 +392,8 @@ void device_bwd(const Layout& L, const void* q, const void* k, const void* v,
     p.dm_unit = static_cast<double*>(scratch_get(st, kScrDm, L.units() * sizeof(double)));
   const bool tensor = !(L.flags & (COTTEN_FLAG_FORCE_GENERIC | COTTEN_FLAG_FP32_PIPE));
   const bool tc_path = tensor && ((L.dtype == COTTEN_F32 && (tc_bwd_supported<float>(p) ||
-                                                              tcf_bwd_supported<float>(p))) ||
+                                                              tcf_bwd_supported<float>(p) ||
+                                                              tcg_bwd_supported<float>(p))) ||
                                   (L.dtype == COTTEN_BF16 && (tcb_bwd_supported<__nv_bfloat16>(p) ||
                                                                tch_bwd_supported<__nv_bfloat16>(p))));
   if (dm_total && tc_path) {  // the tcgen05 kernel's last CTA writes the total (no extra launch)

@@ -1,0 +1,9 @@
+# tch: L2 prefetch distance (items) A/B, both kernels (COTTEN_L2_AHEAD overrides fwd and bwd)
+mkdir -p gpurun_out/tch_l2
+for a in 0 4 8 16; do
+for w in long4k_d128_bf16 sw_n512_d128_bf16; do
+  COTTEN_L2_AHEAD=$a timeout 300 python bench.py --workload $w --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/tch_l2/${w}_a$a.json 2>/dev/null
+  python -c "
+import json; d=json.load(open('gpurun_out/tch_l2/${w}_a$a.json')); k=d['kernels']; print('$w a=$a', round(d['value']), 'fwd %.3f bwd %.3f step %.3f' % (k['fwd_frac'], k['bwd_frac'], k['step_frac']), d['clocks']['sm_mhz'])"
+done
+done
