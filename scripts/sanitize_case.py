@@ -1,7 +1,7 @@
 """One small multi-unit fwd+bwd of a chosen kernel path, for compute-sanitizer
 (memcheck / racecheck / synccheck): python scripts/sanitize_case.py <path>
 with path in tc | tclong | tcf64 | tcflong | tcfmerge | tcb64 | tcbpair |
-tcblong | d32 | rt64 | rt128 | rtbf16 | generic.  Exits non-zero on a
+tcblong | tch | tchlong | tcg | tcglong | d32 | rt64 | rt128 | rtbf16 | generic.  Exits non-zero on a
 parity failure vs the oracle (so a sanitizer run also checks the values)."""
 import sys
 
@@ -25,7 +25,11 @@ B, H, N, D, dt, flags = {
     "tcblong": (2, 2, 1100, 64, torch.bfloat16, 0),   # 9 chunks, flush every 4
     "d32": (160, 2, 50, 32, torch.float32, FP),
     "rt64": (20, 2, 300, 64, torch.float32, FP),
-    "rt128": (8, 2, 300, 128, torch.float32, 0),
+    "rt128": (8, 2, 300, 128, torch.float32, FP),
+    "tch": (160, 2, 300, 128, torch.bfloat16, 0),     # bf16 d_h 128, 5 chunks/unit, >= 2 units/CTA
+    "tchlong": (2, 2, 700, 128, torch.bfloat16, 0),   # 11 chunks, TMEM running-sum flush
+    "tcg": (160, 2, 300, 128, torch.float32, 0),      # fp32 d_h 128, 10 items/pass, >= 2 units/CTA
+    "tcglong": (2, 2, 700, 128, torch.float32, 0),    # 22 items, TMEM running-sum flush
     "rtbf16": (20, 2, 301, 32, torch.bfloat16, 0),    # odd N: register-tiled
     "generic": (6, 2, 70, 24, torch.float32, 0),
 }[path]

@@ -196,15 +196,17 @@ def test_bf16_within_stated_tolerance(D):
     assert_parity(res, oracle_for(res["inputs"], valid, 1.0, 1e-6), valid, "bf16")
 
 
+@pytest.mark.parametrize("flags", [0, _lib.FLAG_FP32_PIPE], ids=["tcgen05", "fp32pipe"])
 @pytest.mark.parametrize("D", [64, 128])
 @pytest.mark.parametrize("N", [7, 33, 64, 65, 200, 513, 1000, 4096])
-def test_head_dim_64_128_seq_lens_f32(D, N):
-    """kernels_rt.cuh (register-tiled FP32 pipe): tile edges (TR = 64 / 32
-    rows), the 512-row running-sum flush, left-padded masks."""
+def test_head_dim_64_128_seq_lens_f32(D, N, flags):
+    """Both paths at d_h 64 / 128: the tensor-core kernels (kernels_tcf.cuh,
+    kernels_tcg.cuh) and kernels_rt.cuh (register-tiled FP32 pipe, tile edges
+    TR = 64 / 32 rows); the 512-row running-sum flush, left-padded masks."""
     B, H = (3, 2) if N <= 1000 else (2, 1)
     h = inputs.make_host(B, H, N, D, seed=N + D)
     valid = inputs.left_padded_mask(B, N, N)
-    res = run_gpu(h, valid, 0.75, 1e-6, "f32")
+    res = run_gpu(h, valid, 0.75, 1e-6, "f32", flags)
     assert_parity(res, oracle_for(res["inputs"], valid, 0.75, 1e-6), valid, "f32")
 
 
@@ -245,15 +247,17 @@ def test_head_dim_128_random_mask(dtype):
     assert_parity(res, oracle_for(res["inputs"], valid, 1.0, 1e-6), valid, dtype)
 
 
+@pytest.mark.parametrize("flags", [0, _lib.FLAG_FP32_PIPE], ids=["default", "fp32pipe"])
 @pytest.mark.parametrize("D", [32, 64, 128])
 @pytest.mark.parametrize("N", [5, 129, 1000])
-def test_bf16_register_tiled_seq_lens(D, N):
-    """bf16 in HBM on kernels_rt.cuh (d_h 32 / 64 / 128): tile edges of the
-    128 / 64 / 32-row tiles, random masks."""
+def test_bf16_register_tiled_seq_lens(D, N, flags):
+    """bf16 in HBM on kernels_rt.cuh (d_h 32 / 64 / 128, FP32_PIPE: tile edges
+    of the 128 / 64 / 32-row tiles) and on the default path (the tensor-core
+    kernels where the shape allows), random masks."""
     B, H = 3, 2
     h = inputs.make_host(B, H, N, D, seed=7 * N + D)
     valid = inputs.random_mask(B, N, N + D)
-    res = run_gpu(h, valid, 1.0, 1e-6, "bf16")
+    res = run_gpu(h, valid, 1.0, 1e-6, "bf16", flags)
     assert_parity(res, oracle_for(res["inputs"], valid, 1.0, 1e-6), valid, "bf16")
 
 
