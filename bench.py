@@ -61,10 +61,10 @@ WORKLOADS = {
                 "left-padded mask"),
     "long4k_d64": (512, 4096, 1, 64, 1, True,
                    "BASELINE config #5 point: cosine-attn fwd+bwd, N=4096, H=1, d_h=64, B=512, fp32 "
-                   "(register-tiled FP32-pipe kernels), left-padded mask"),
+                   "(three-part tcgen05 kernels), left-padded mask"),
     "long4k_d128": (256, 4096, 1, 128, 1, True,
                     "BASELINE config #5 point: cosine-attn fwd+bwd, N=4096, H=1, d_h=128, B=256, fp32 "
-                    "(register-tiled FP32-pipe kernels), left-padded mask"),
+                    "(three-part tcgen05 kernels), left-padded mask"),
 }
 # bf16 in HBM (fp32 arithmetic) points of config #5: the same shapes, half the bytes
 for _name in ("long4k", "long4k_d64", "long4k_d128"):
