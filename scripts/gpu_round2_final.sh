@@ -3,7 +3,7 @@
 rm -rf gpurun_out/final gpurun_out/sweep
 mkdir -p gpurun_out/final
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/final/gpu.csv 2>&1
-timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/final/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/final/pytest_gpu.log
+timeout 2400 python -m pytest tests -q -m gpu --timeout 600 -p no:cacheprovider > gpurun_out/final/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/final/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/final/smoke.log
 timeout 900 python bench.py > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/final/bench_ref.json 2>> gpurun_out/final/bench.err
