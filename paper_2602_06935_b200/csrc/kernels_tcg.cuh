@@ -223,6 +223,68 @@ __device__ __forceinline__ void stage_block(uint8_t* T, int row, int q, const fl
 // ======================================================================================
 // Forward
 // ======================================================================================
+// Pass 2 reads Q alone, so its items are 64 rows (raw fp32 as four 64-row
+// boxes over X | Y = 32 KB, the three parts over X | Y and the part-2 area =
+// 48 KB) and the row-output MMAs are full M = 64 ones; pass 1 keeps the
+// 32-row (K, V) items.
+constexpr int kRowsQ = 64;
+constexpr uint32_t kBoxQ = 8192;   // 64 rows x 128 B
+constexpr uint32_t kPartQ = 2 * kBoxQ;
+// item i of this CTA's schedule: unit index j (0, 1, ...), pass, chunk
+__device__ __forceinline__ bool fwd_item(int i, int P, int C1, int C2, int units, int& u, int& ps, int& c) {
+  const int per = C1 + (P == 2 ? C2 : 0);
+  const int jj = i / per, rem = i - jj * per;
+  u = blockIdx.x + jj * gridDim.x;
+  if (u >= units) return false;
+  ps = rem >= C1;
+  c = ps ? rem - C1 : rem;
+  return true;
+}
+// Q splitter: four threads per 64-row tile row (32 columns each) at lanes
+// rr + 8 q4 (row 8 warp + rr): an 8-lane LDS.128 phase is eight rows of one box
+__device__ __forceinline__ void split_q(uint8_t* X, int t, float eps, int r, int N, float* norms) {
+  const int lane = t & 31, q4 = lane >> 3, row = 8 * (t >> 5) + (lane & 7);
+  float x[32];
+  const uint8_t* box = X + q4 * kBoxQ;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4 v = *reinterpret_cast<const float4*>(box + goff(row, k));
+    x[4 * k] = v.x;
+    x[4 * k + 1] = v.y;
+    x[4 * k + 2] = v.z;
+    x[4 * k + 3] = v.w;
+  }
+  float a = 0.f, b = 0.f;
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    a = fmaf(x[e], x[e], a);
+    b = fmaf(x[e + 1], x[e + 1], b);
+  }
+  float ss = a + b;
+  ss += __shfl_xor_sync(0xffffffffu, ss, 8);
+  ss += __shfl_xor_sync(0xffffffffu, ss, 16);
+  const float iv = rsqrtf(ss + eps);
+  r += row;
+  if (norms && r < N && q4 == 0) norms[r] = (ss + eps) * iv;  // q~ every row (:366-377)
+#pragma unroll
+  for (int e = 0; e < 32; ++e) x[e] *= iv;
+  __syncwarp();  // the row's four threads have read its raw boxes
+  uint8_t* h0 = X + (q4 >> 1) * kBoxQ;
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+    store_parts8(h0, h0 + kPartQ, h0 + 2 * kPartQ, row, 4 * (q4 & 1) + g, x + 8 * g);
+}
+// O (64 x 128) = Q~ (64-row three-part tile, K-major) x S (three state parts, MN-major)
+__device__ __forceinline__ void issue_rowout_q(uint32_t d, const uint32_t (&a)[3], const uint32_t (&b)[3]) {
+  const uint32_t id = idesc_bf16(64, 128, false, true);
+#pragma unroll 1
+  for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+    for (int pr = 0; pr < 6; ++pr)
+      mma_bf16(d, sdesc(a[part_i(pr)] + (uint32_t)(kk >> 2) * kBoxQ + 32u * (kk & 3), 16u, 1024u),
+               state_desc<true>(b[part_j(pr)], kk), id, (kk == 0 && pr == 0) ? 0u : 1u);
+}
+
 __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
@@ -230,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = (int)p.N, H = (int)p.H;
   const int units = (int)(p.B * p.H);
-  const int C = (N + kRows - 1) / kRows;
+  const int C1 = (N + kRows - 1) / kRows, C2 = (N + kRowsQ - 1) / kRowsQ;
   const int P = (p.out != nullptr || p.saved_norms != nullptr) ? 2 : 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Bars* br = reinterpret_cast<Bars*>(smem + kOffBar);
@@ -250,14 +312,20 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = u / H, h = u - b * H;
         for (int ps = 0; ps < P; ++ps)
-          for (int c = 0; c < C; ++c, ++it) {
+          for (int c = 0; c < (ps ? C2 : C1); ++c, ++it) {
             const int st = slot2(it);
-            tc::ItemPos f;
-            if (p.l2_ahead && tc::item_pos(it + p.l2_ahead, P, C, units, H, f))
+            int fu, fps, fc;
+            if (p.l2_ahead && fwd_item(it + p.l2_ahead, P, C1, C2, units, fu, fps, fc)) {
+              const int fb = fu / H, fh = fu - fb * H;
               for (int hb = 0; hb < 4; ++hb) {
-                tc::tma_prefetch_4d(f.ps == 0 ? &tk : &tq, 32 * hb, f.c * kRows, f.h, f.b);
-                if (f.ps == 0) tc::tma_prefetch_4d(&tv, 32 * hb, f.c * kRows, f.h, f.b);
+                if (fps == 0) {
+                  tc::tma_prefetch_4d(&tk, 32 * hb, fc * kRows, fh, fb);
+                  tc::tma_prefetch_4d(&tv, 32 * hb, fc * kRows, fh, fb);
+                } else {
+                  tc::tma_prefetch_4d(&tq, 32 * hb, fc * kRowsQ, fh, fb);
+                }
               }
+            }
             mbar_wait(&br->slot_free[st], par2(it) ^ 1u);
             uint8_t* X = smem + kOffRing + st * kSlot;
             if (ps == 0) {
@@ -266,10 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
                 tma_load_4d(X + hb * kBox, &tk, 32 * hb, c * kRows, h, b, &br->raw_full[st]);
                 tma_load_4d(X + kRaw + hb * kBox, &tv, 32 * hb, c * kRows, h, b, &br->raw_full[st]);
               }
-            } else {
-              mbar_expect_tx(&br->raw_full[st], kRaw);
+            } else {  // Q: four 64-row boxes over X | Y
+              mbar_expect_tx(&br->raw_full[st], 4 * kBoxQ);
               for (int hb = 0; hb < 4; ++hb)
-                tma_load_4d(X + hb * kBox, &tq, 32 * hb, c * kRows, h, b, &br->raw_full[st]);
+                tma_load_4d(X + hb * kBoxQ, &tq, 32 * hb, c * kRowsQ, h, b, &br->raw_full[st]);
             }
           }
       }
@@ -281,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
     const uint32_t opS[3] = {base + kOffOps, base + kOffOps + kStatePart, base + kOffOps + 2 * kStatePart};
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       for (int ps = 0; ps < P; ++ps)
-        for (int c = 0; c < C; ++c, ++it) {
+        for (int c = 0; c < (ps ? C2 : C1); ++c, ++it) {
           const int st = slot2(it);
           mbar_wait(&br->split_full[st], par2(it));
           if (ps == 0 && c == 0 && P == 1 && j > 0) mbar_wait(&br->op_ready, (j - 1) & 1);
@@ -291,14 +359,15 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
           if (ps == 1) take_out(br, par, b);
           tc_fence_after();
           const uint32_t X = base + kOffRing + st * kSlot;
-          const uint32_t xp[3] = {X, X + kPart, X + 2 * kRaw};
-          const uint32_t yp[3] = {X + kRaw, X + kRaw + kPart, X + 2 * kRaw + kPart};
           if (elect_one()) {
             if (ps == 0) {  // S += K~^T V (attention.cpp:345-353)
+              const uint32_t xp[3] = {X, X + kPart, X + 2 * kRaw};
+              const uint32_t yp[3] = {X + kRaw, X + kRaw + kPart, X + 2 * kRaw + kPart};
               const int ks = (min(kRows, N - c * kRows) + 15) >> 4;
               issue_red(tmem + kAcc, xp, yp, ks, c % kFlush == 0);
             } else {  // O = Q~ S (:379-387)
-              issue_rowout<true>(tmem + out_col(b), xp, opS);
+              const uint32_t qp[3] = {X, X + kPartQ, X + 2 * kPartQ};
+              issue_rowout_q(tmem + out_col(b), qp, opS);
             }
             mma_commit(&br->mma_done[st]);
           }
@@ -314,12 +383,12 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = u / H, h = u - b * H;
         for (int ps = 0; ps < P; ++ps)
-          for (int c = 0; c < C; ++c, ++it) {
+          for (int c = 0; c < (ps ? C2 : C1); ++c, ++it) {
             const int st = slot2(it);
             mbar_wait(&br->staged[st], par2(it));
-            if (ps == 1 && p.out) {  // O staged in Y (unused in pass 2)
-              uint8_t* Y = smem + kOffRing + st * kSlot + kRaw;
-              for (int hb = 0; hb < 4; ++hb) tma_store_4d(&to, Y + hb * kBox, 32 * hb, c * kRows, h, b);
+            if (ps == 1 && p.out) {  // O staged as four 64-row fp32 boxes over X | Y
+              uint8_t* X = smem + kOffRing + st * kSlot;
+              for (int hb = 0; hb < 4; ++hb) tma_store_4d(&to, X + hb * kBoxQ, 32 * hb, c * kRowsQ, h, b);
               bulk_wait_read0();
             }
             mbar_arrive(&br->slot_free[st]);
@@ -342,21 +411,21 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
       float* norms = norms_all ? norms_all + (int64_t)u * 2 * N : nullptr;
       mbar_wait(&br->fl_full[sl], (j >> 1) & 1);
       const UnitConst uc = ucs[sl];
-      for (int k = 0; k < P * C; ++k, ++it) {
-        const int ps = k >= C, c = ps ? k - C : k;
+      const int items = C1 + (P == 2 ? C2 : 0);
+      for (int k = 0; k < items; ++k, ++it) {
+        const int ps = k >= C1, c = ps ? k - C1 : k;
         const int st = slot2(it);
         uint8_t* X = smem + kOffRing + st * kSlot;
         uint8_t* Y = X + kRaw;
         if (splitter) {  // ---------------- splitter ----------------
           mbar_wait(&br->raw_full[st], par2(it));
-          SplitRow s;
-          split_load(X, t, s);
-          const int r = c * kRows + s.row;
-          const bool wr = norms && r < N && s.qb == 0;
-          const float iv = rsqrtf(s.ss + eps);
           if (ps == 0) {  // k~ masked (attention.cpp:334-343), V as it is
+            SplitRow s;
+            split_load(X, t, s);
+            const int r = c * kRows + s.row;
+            const float iv = rsqrtf(s.ss + eps);
             const bool f = r < N && tc::flag_at(fl, r);
-            if (wr) norms[N + r] = f ? (s.ss + eps) * iv : 1.0f;
+            if (norms && r < N && s.qb == 0) norms[N + r] = f ? (s.ss + eps) * iv : 1.0f;
 #pragma unroll
             for (int e = 0; e < 16; ++e) s.x[e] = f ? s.x[e] * iv : 0.f;  // NaN-safe zeros
             SplitRow v;
@@ -364,12 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
             __syncwarp();
             split_store(X, X + 2 * kRaw, s);
             split_store(Y, X + 2 * kRaw + kPart, v);
-          } else {  // q~ every row (:366-377)
-            if (wr) norms[r] = (s.ss + eps) * iv;
-#pragma unroll
-            for (int e = 0; e < 16; ++e) s.x[e] *= iv;
-            __syncwarp();
-            split_store(X, X + 2 * kRaw, s);
+          } else {
+            split_q(X, t, eps, c * kRowsQ, N, norms);
           }
           fence_proxy_async();
           __syncwarp();
@@ -379,17 +444,17 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
           tc_fence_after();
           if (ps == 0) {
             arrive_staged(br, st, lane);  // a pass-1 item stages nothing: free the slot now
-            if (c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
+            if (c != C1 - 1 && c % kFlush == kFlush - 1) {  // long N: flush the accumulator
               flush_acc(tmem, lane_base, c == kFlush - 1);
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&br->acc_free);
             }
-            if (c == C - 1) {  // S complete: saved S + the three part tiles
+            if (c == C1 - 1) {  // S complete: saved S + the three part tiles
 #pragma unroll 1
               for (int q = 0; q < 4; ++q) {
                 float sv[32];
-                acc_block(tmem, lane_base, q, C > kFlush, sv);
+                acc_block(tmem, lane_base, q, C1 > kFlush, sv);
                 if (gS_all) {
                   float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * (kD * kD) + t * kD + 32 * q);
 #pragma unroll
@@ -403,19 +468,19 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcg_kernel(
               epi_sync();
               if (t == 0) mbar_arrive(&br->op_ready);
             }
-          } else {  // O rows = s (Q~ S), staged in Y as four fp32 boxes
+          } else {  // O rows = s (Q~ S), staged as four 64-row fp32 boxes over X | Y
             const int b = n1 & 1;
-            if (wq < 2) {
-              const int row = 16 * wq + (lane & 15), h = lane >> 4;
-              const uint32_t D = tmem + out_col(b) + lane_base;
+            const int row = 16 * wq + (lane & 15), h = lane >> 4;
+            const uint32_t D = tmem + out_col(b) + lane_base;
 #pragma unroll 1
-              for (int hh = 0; hh < 2; ++hh) {
-                float o[32];
-                tmem_ld_pair(D + 64u * hh, o);
+            for (int hh = 0; hh < 2; ++hh) {
+              float o[32];
+              tmem_ld_pair(D + 64u * hh, o);
+              const int q = 2 * hh + h;
 #pragma unroll
-                for (int e = 0; e < 32; ++e) o[e] *= uc.s;
-                stage_block(Y, row, 2 * hh + h, o);
-              }
+              for (int k2 = 0; k2 < 8; ++k2)
+                *reinterpret_cast<float4*>(X + q * kBoxQ + goff(row, k2)) =
+                    make_float4(o[4 * k2] * uc.s, o[4 * k2 + 1] * uc.s, o[4 * k2 + 2] * uc.s, o[4 * k2 + 3] * uc.s);
             }
             release_out(br, b, lane);
             ++n1;
@@ -752,12 +817,12 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcg_kernel(
 // ---- host side ----------------------------------------------------------------------
 
 // 4-D fp32 map over (128, N, H, B), box (32, 32, 1, 1), 128-byte swizzle: four boxes per row
-inline bool make_tcg_map(CUtensorMap* map, const void* base, const OpParams& p) {
+inline bool make_tcg_map(CUtensorMap* map, const void* base, const OpParams& p, int rows = tcg::kRows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[4] = {128, (cuuint64_t)p.N, (cuuint64_t)p.H, (cuuint64_t)p.B};
   cuuint64_t strides[3] = {(cuuint64_t)p.sn * 4, (cuuint64_t)p.sh * 4, (cuuint64_t)p.sb * 4};
-  cuuint32_t box[4] = {32, (cuuint32_t)tcg::kRows, 1, 1};
+  cuuint32_t box[4] = {32, (cuuint32_t)rows, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -804,8 +869,8 @@ inline cudaError_t launch_tcg_pdl(void (*kern)(KArgs...), int grid, cudaStream_t
 }
 inline int launch_tcg_fwd(const OpParams& p, cudaStream_t st) {
   CUtensorMap mq, mk, mv, mo;
-  if (!make_tcg_map(&mq, p.q, p) || !make_tcg_map(&mk, p.k, p) || !make_tcg_map(&mv, p.v, p) ||
-      !make_tcg_map(&mo, p.out ? p.out : p.q, p))
+  if (!make_tcg_map(&mq, p.q, p, tcg::kRowsQ) || !make_tcg_map(&mk, p.k, p) || !make_tcg_map(&mv, p.v, p) ||
+      !make_tcg_map(&mo, p.out ? p.out : p.q, p, tcg::kRowsQ))
     return -1;
   if (cudaFuncSetAttribute(tcg::cos_fwd_tcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tcg::kSmemBytes) != cudaSuccess)
