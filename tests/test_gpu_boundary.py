@@ -131,7 +131,7 @@ def _host_inputs(B, H, N, D, seed, dtype="f32"):
 
 
 @pytest.mark.parametrize("D,dtype,N", [(32, "f32", 200), (64, "f32", 300), (32, "bf16", 256),
-                                       (32, "f32", 50)])
+                                       (32, "f32", 50), (128, "f32", 300), (128, "bf16", 256)])
 def test_cached_host_pair_equals_uncached_host_pair(D, dtype, N):
     """cotten_fwd_host_cached / cotten_bwd_host_cached (the AttentionCache kept on
     the device) give bit-identical outputs to cotten_fwd_host / cotten_bwd_host."""

@@ -128,3 +128,12 @@ def test_tch_forward_only_without_outputs(N):
     ops.forward(t["q"], t["k"], t["v"], vm, 1.0, saved_S=S2)
     torch.cuda.synchronize()
     assert torch.equal(S, S2)
+
+
+def test_tch_strided_projection_layout():
+    """[B][N][H][D] storage (stride_n = H*D): the projection output read in place."""
+    B, H, N = 4, 2, 300
+    h = inputs.make_host(B, H, N, D, seed=9)
+    valid = inputs.random_mask(B, N, 9)
+    a = run_gpu(h, valid, 1.0, 1e-6, "bf16", layout="bnhd")
+    assert_parity(a, oracle_for(a["inputs"], valid, 1.0, 1e-6), valid, "bf16")
