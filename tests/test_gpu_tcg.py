@@ -125,3 +125,12 @@ def test_tcg_saved_norms_and_state():
             np.testing.assert_allclose(got[b * H + hh, 1], r["norm_k"], rtol=1e-6)
             assert np.all(got[b * H + hh, 1][valid[b] == 0] == 1.0)
             assert normwise(gS[b * H + hh][None, None], r["S"][None, None]) <= 1e-5
+
+
+@pytest.mark.parametrize("N", [50, 300])
+def test_tcg_no_mask(N):
+    """valid = NULL: every row valid (attention_forward without a RowMask)."""
+    B, H = 6, 2
+    h = inputs.make_host(B, H, N, D, seed=N + 31)
+    res = run_gpu(h, None, 0.75, 1e-6, "f32")
+    assert_parity(res, oracle_for(res["inputs"], None, 0.75, 1e-6), None, "f32")

@@ -137,3 +137,12 @@ def test_tch_strided_projection_layout():
     valid = inputs.random_mask(B, N, 9)
     a = run_gpu(h, valid, 1.0, 1e-6, "bf16", layout="bnhd")
     assert_parity(a, oracle_for(a["inputs"], valid, 1.0, 1e-6), valid, "bf16")
+
+
+@pytest.mark.parametrize("N", [50, 300])
+def test_tch_no_mask(N):
+    """valid = NULL: every row valid (attention_forward without a RowMask)."""
+    B, H = 6, 2
+    h = inputs.make_host(B, H, N, D, seed=N + 31)
+    res = run_gpu(h, None, 0.75, 1e-6, "bf16")
+    assert_parity(res, oracle_for(res["inputs"], None, 0.75, 1e-6), None, "bf16")
