@@ -30,6 +30,8 @@ B, H, N, D, dt, flags = {
     "tchlong": (2, 2, 700, 128, torch.bfloat16, 0),   # 11 chunks, TMEM running-sum flush
     "tcg": (160, 2, 300, 128, torch.float32, 0),      # fp32 d_h 128, 10 items/pass, >= 2 units/CTA
     "tcglong": (2, 2, 700, 128, torch.float32, 0),    # 22 items, TMEM running-sum flush
+    "tchsmall": (2, 2, 200, 128, torch.bfloat16, 0),  # racecheck-sized
+    "tcgsmall": (2, 2, 200, 128, torch.float32, 0),
     "rtbf16": (20, 2, 301, 32, torch.bfloat16, 0),    # odd N: register-tiled
     "generic": (6, 2, 70, 24, torch.float32, 0),
 }[path]
