@@ -314,6 +314,25 @@ __device__ __forceinline__ void acc_half(uint32_t tmem, const float* run, int wq
     }
   }
 }
+// Half h = lane / 16 (columns 32 h ..) of accumulator row 16 wq + lane % 16 for
+// all 32 lanes at once (tcgen05.ld.16x32bx2), plus the flushed running sum:
+// the per-unit S / G epilogue runs on all 128 epiloguer threads.
+__device__ __forceinline__ void acc_pair(uint32_t tmem, const float* run, int wq, int lane,
+                                         bool with_run, float (&r)[32]) {
+  tmem_ld_pair(tmem + ((uint32_t)(32 * wq) << 16), r);
+  if (with_run) {
+    const int l = lane & 15, h = lane >> 4;
+    const float4* rr = reinterpret_cast<const float4*>(run + (16 * wq + l) * 64);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = rr[(8 * h + k) ^ l];
+      r[4 * k] += v.x;
+      r[4 * k + 1] += v.y;
+      r[4 * k + 2] += v.z;
+      r[4 * k + 3] += v.w;
+    }
+  }
+}
 __device__ __forceinline__ void flush_acc(uint32_t tmem, float* run, int wq, int lane, bool first) {
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
@@ -553,40 +572,29 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcf_kernel(
               __syncwarp();
               if (lane == 0) mbar_arrive(&br->acc_free);
             }
-            if (kMerge && c == C - 1) {  // the two heads' S: diagonal blocks, operand blockdiag
-              const int hh = wq >> 1;  // rows 0-31: first head (columns 0-31), 32-63: second
+            if (c == C - 1) {  // S complete: saved S + its three part tiles (all 128 threads)
+              const int a = 16 * wq + (lane & 15), h = lane >> 4;  // row a, columns 32 h ..
               float sv[32];
-              acc_half(tmem, run, wq, lane, hh, C > kFlush, sv);
-              if (lane < 16) {
-                const int a = 16 * wq + lane;
-                if (gS_all) {
-                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)(up.g + hh) * 1024 + (a & 31) * 32);
+              acc_pair(tmem, run, wq, lane, C > kFlush, sv);
+              if (kMerge) {  // the two heads' S: diagonal blocks, operand blockdiag
+                const bool live = h == (a >> 5);  // rows 0-31: first head (columns 0-31), 32-63: second
+                if (live && gS_all) {
+                  float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)(up.g + h) * 1024 + (a & 31) * 32);
 #pragma unroll
                   for (int e = 0; e < 8; ++e)
                     gs[e] = make_float4(sv[4 * e], sv[4 * e + 1], sv[4 * e + 2], sv[4 * e + 3]);
                 }
-                float z[32];
+                if (!live) {
 #pragma unroll
-                for (int e = 0; e < 32; ++e) z[e] = 0.f;
-                store_state_half(ops, a, hh, sv);
-                store_state_half(ops, a, hh ^ 1, z);
-              }
-            } else if (c == C - 1) {  // S complete: saved S + its three part tiles
-#pragma unroll 1
-              for (int h = 0; h < 2; ++h) {
-                float sv[32];
-                acc_half(tmem, run, wq, lane, h, C > kFlush, sv);
-                if (lane < 16) {
-                  const int a = 16 * wq + lane;
-                  if (gS_all) {
-                    float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 32 * h);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                      gs[e] = make_float4(sv[4 * e], sv[4 * e + 1], sv[4 * e + 2], sv[4 * e + 3]);
-                  }
-                  store_state_half(ops, a, h, sv);
+                  for (int e = 0; e < 32; ++e) sv[e] = 0.f;
                 }
+              } else if (gS_all) {
+                float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 32 * h);
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  gs[e] = make_float4(sv[4 * e], sv[4 * e + 1], sv[4 * e + 2], sv[4 * e + 3]);
               }
+              store_state_half(ops, a, h, sv);
             }
             if (c == C - 1) {
               fence_proxy_async();
@@ -807,31 +815,28 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcf_kernel(
             mbar_wait(&br->red_done, j & 1);
             tc_fence_after();
             float dotf = 0.f;
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-              // kMerge: only the diagonal blocks (rows 0-31 x columns 0-31: the first
-              // head's G, rows 32-63 x columns 32-63: the second's); the operand is
-              // blockdiag(s G_h, s G_h+1)
-              const bool live = !kMerge || h == (wq >> 1);
+            {
+              // all 128 threads: row a, columns 32 h ..; kMerge: only the diagonal
+              // blocks (rows 0-31 x columns 0-31: the first head's G, rows 32-63 x
+              // columns 32-63: the second's); the operand is blockdiag(s G_h, s G_h+1)
+              const int a = 16 * wq + (lane & 15), h = lane >> 4;
+              const bool live = !kMerge || h == (a >> 5);
               float gr[32];
-              acc_half(tmem, run, wq, lane, h, C > kFlush, gr);
+              acc_pair(tmem, run, wq, lane, C > kFlush, gr);
               if (!live) {
 #pragma unroll
                 for (int e = 0; e < 32; ++e) gr[e] = 0.f;
               }
-              if (lane < 16) {
-                const int a = 16 * wq + lane;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  float sv[8];
-                  load_parts8(ops, ops + kBox, ops + 2 * kBox, a, 4 * h + q, sv);
+              for (int q = 0; q < 4; ++q) {
+                float sv[8];
+                load_parts8(ops, ops + kBox, ops + 2 * kBox, a, 4 * h + q, sv);
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) dotf = fmaf(gr[8 * q + e], sv[e], dotf);
-                }
-#pragma unroll
-                for (int e = 0; e < 32; ++e) gr[e] *= uc.s;
-                store_state_half(ops + 3 * kBox, a, h, gr);
+                for (int e = 0; e < 8; ++e) dotf = fmaf(gr[8 * q + e], sv[e], dotf);
               }
+#pragma unroll
+              for (int e = 0; e < 32; ++e) gr[e] *= uc.s;
+              store_state_half(ops + 3 * kBox, a, h, gr);
             }
             double dot = (double)dotf;
 #pragma unroll
