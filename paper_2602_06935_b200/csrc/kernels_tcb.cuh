@@ -361,6 +361,35 @@ __device__ __forceinline__ void flush_acc(uint32_t tmem, float* run, int wq, int
     }
   }
 }
+// Half h = lane / 16 (columns 32 h ..) of accumulator row 16 wq + lane % 16 for
+// all 32 lanes at once (tcgen05.ld.16x32bx2), plus the flushed running sum: the
+// per-unit S / G epilogue of the d_h = 64 kernels runs on all 128 threads.
+__device__ __forceinline__ void acc_pair(uint32_t tmem, const float* run, int wq, int lane,
+                                         bool with_run, float (&r)[32]) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(r);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], 32;"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+        "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+        "=r"(u[14]), "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]),
+        "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]),
+        "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+      : "r"(tmem + ((uint32_t)(32 * wq) << 16)));
+  tmem_wait_ld();
+  if (with_run) {
+    const int l = lane & 15, h = lane >> 4;
+    const float4* rr = reinterpret_cast<const float4*>(run + (16 * wq + l) * 64);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = rr[(8 * h + k) ^ l];
+      r[4 * k] += v.x;
+      r[4 * k + 1] += v.y;
+      r[4 * k + 2] += v.z;
+      r[4 * k + 3] += v.w;
+    }
+  }
+}
 // <x, hi + lo> over half h of row a of a state tile pair
 __device__ __forceinline__ float dot_state_half(const uint8_t* hi, const uint8_t* lo, int a, int h,
                                                 const float (&x)[32]) {
@@ -620,21 +649,16 @@ __global__ void __launch_bounds__(kThreads, 1) cos_fwd_tcb_kernel(
               epi_sync();
               if (t == 0) mbar_arrive(&br->op_ready);
             } else if (c == C - 1) {  // S complete: saved S + the bf16 hi / lo state operand
-#pragma unroll 1
-              for (int h = 0; h < 2; ++h) {
-                float sv[32];
-                acc_half(tmem, run, wq, lane, h, C > kFlush, sv);
-                if (lane < 16) {
-                  const int a = 16 * wq + lane;
-                  if (gS_all) {
-                    float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 32 * h);
+              const int a = 16 * wq + (lane & 15), h = lane >> 4;  // all 128 threads
+              float sv[32];
+              acc_pair(tmem, run, wq, lane, C > kFlush, sv);
+              if (gS_all) {
+                float4* gs = reinterpret_cast<float4*>(gS_all + (int64_t)u * 4096 + a * 64 + 32 * h);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                      gs[e] = make_float4(sv[4 * e], sv[4 * e + 1], sv[4 * e + 2], sv[4 * e + 3]);
-                  }
-                  store_split_half(ops, ops + kStateTile, a, h, sv);
-                }
+                for (int e = 0; e < 8; ++e)
+                  gs[e] = make_float4(sv[4 * e], sv[4 * e + 1], sv[4 * e + 2], sv[4 * e + 3]);
               }
+              store_split_half(ops, ops + kStateTile, a, h, sv);
               fence_proxy_async();
               tc_fence_before();
               epi_sync();
@@ -868,19 +892,14 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcb_kernel(
                 for (int e = 0; e < 32; ++e) gr[e] *= uc.s;
                 store_blockdiag(ops + 2 * kStateTile, ops + 3 * kStateTile, a, gr);
               }
-            } else {
-#pragma unroll 1
-              for (int h = 0; h < 2; ++h) {
-                float gr[32];
-                acc_half(tmem, run, wq, lane, h, C > kFlush, gr);
-                if (lane < 16) {
-                  const int a = 16 * wq + lane;
-                  dotf += dot_state_half(ops, ops + kStateTile, a, h, gr);
+            } else {  // all 128 threads: row a, columns 32 h ..
+              const int a = 16 * wq + (lane & 15), h = lane >> 4;
+              float gr[32];
+              acc_pair(tmem, run, wq, lane, C > kFlush, gr);
+              dotf = dot_state_half(ops, ops + kStateTile, a, h, gr);
 #pragma unroll
-                  for (int e = 0; e < 32; ++e) gr[e] *= uc.s;
-                  store_split_half(ops + 2 * kStateTile, ops + 3 * kStateTile, a, h, gr);
-                }
-              }
+              for (int e = 0; e < 32; ++e) gr[e] *= uc.s;
+              store_split_half(ops + 2 * kStateTile, ops + 3 * kStateTile, a, h, gr);
             }
             double dot = (double)dotf;
 #pragma unroll
