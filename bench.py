@@ -784,12 +784,12 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
             raise errs[0]
 
     run(max(args.warmup, 3))
-    # K steps, timed R times (COTTEN_E2E_REPEATS, default 5); the median repeat is the
+    # K steps, timed R times (COTTEN_E2E_REPEATS, default 7); the median repeat is the
     # value.  One K-step window is tens of ms of host wall clock, so a single window is
     # at the mercy of host scheduling on the box (single windows of the same run have
     # read anywhere from 20 k to 70 k seq/s at ML-1M).
     reps = []
-    for _ in range(max(1, int(os.environ.get("COTTEN_E2E_REPEATS", "5")))):
+    for _ in range(max(1, int(os.environ.get("COTTEN_E2E_REPEATS", "7")))):
         barrier(world)
         t0 = time.perf_counter()
         run(args.steps)
