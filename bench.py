@@ -784,6 +784,12 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
             raise errs[0]
 
     run(max(args.warmup, 3))
+    # untimed warm-up of the copy path itself (at least 0.5 s of transfers): on a
+    # freshly started box the first windows of PCIe traffic ran slow once (22 k / 37 k,
+    # then 69 k seq/s); the windows still scatter with the shared node's host / PCIe load
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 0.5:
+        run(max(args.warmup, 3))
     # K steps, timed R times (COTTEN_E2E_REPEATS, default 7); the median repeat is the
     # value.  One K-step window is tens of ms of host wall clock, so a single window is
     # at the mercy of host scheduling on the box (single windows of the same run have
