@@ -736,9 +736,12 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
         Ls.append(t)
 
     # The reference calls the op from parallel_chunks workers (encoder.cpp:295,345); the
-    # host entry points are thread-safe with per-thread streams, so W host threads each
-    # run the step on a contiguous slice of the batch and their PCIe transfers overlap.
-    W = max(1, min(B, int(os.environ.get("COTTEN_E2E_THREADS", "2"))))
+    # host entry points are thread-safe with per-thread streams, so W host threads
+    # (COTTEN_E2E_THREADS) can each run the step on a contiguous slice of the batch.
+    # Default 1: one thread reads 64 k seq/s in every window on a box where the raw
+    # PCIe copies are steady, while 2 threads scattered between 27 k and 70 k across
+    # boxes (profiles/r02an_e2e_threads); the call already pipelines its own slices.
+    W = max(1, min(B, int(os.environ.get("COTTEN_E2E_THREADS", "1"))))
     es = 2 if dname == "bf16" else 4
     per = (B + W - 1) // W
     slices = [(b0, min(B, b0 + per)) for b0 in range(0, B, per)]
