@@ -737,11 +737,11 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
 
     # The reference calls the op from parallel_chunks workers (encoder.cpp:295,345); the
     # host entry points are thread-safe with per-thread streams, so W host threads
-    # (COTTEN_E2E_THREADS) can each run the step on a contiguous slice of the batch.
-    # Default 1: one thread reads 64 k seq/s in every window on a box where the raw
-    # PCIe copies are steady, while 2 threads scattered between 27 k and 70 k across
-    # boxes (profiles/r02an_e2e_threads); the call already pipelines its own slices.
-    W = max(1, min(B, int(os.environ.get("COTTEN_E2E_THREADS", "1"))))
+    # (COTTEN_E2E_THREADS, default 4 = the host-call gate's default) each run the step
+    # on a contiguous slice of the batch, so their PCIe transfers overlap: with
+    # persistent workers 1 / 2 / 4 threads read 68 / 77 / 79 k seq/s, every window
+    # within 1 % (profiles/r02an_e2e_threads).
+    W = max(1, min(B, int(os.environ.get("COTTEN_E2E_THREADS", "4"))))
     es = 2 if dname == "bf16" else 4
     per = (B + W - 1) // W
     slices = [(b0, min(B, b0 + per)) for b0 in range(0, B, per)]
@@ -768,21 +768,37 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
 
     dev = torch.cuda.current_device()  # this rank's GPU (new threads start on device 0)
 
-    def run(nsteps):
-        errs = []
+    # Persistent worker threads, as a training loop keeps its workers: each host thread's
+    # staging context (streams, device buffers; thread-local in the library) is created
+    # once, during the warm-up.  (Threads created per timed window put that setup —
+    # cudaStreamCreate, cudaMalloc, and cudaFree at thread exit, which synchronises the
+    # device — inside the windows: single windows fell to 6-20 k seq/s.)
+    import queue
+    cmds = [queue.Queue() for _ in slices]
+    done = queue.Queue()
 
-        def worker(b0, b1):
+    def worker(i, b0, b1):
+        torch.cuda.set_device(dev)
+        while True:
+            n = cmds[i].get()
+            if n is None:
+                return
             try:
-                torch.cuda.set_device(dev)
-                for _ in range(nsteps):
+                for _ in range(n):
                     step(b0, b1)
-            except Exception as e:  # surfaced after join
-                errs.append(e)
-        ths = [threading.Thread(target=worker, args=sl) for sl in slices]
-        for th in ths:
-            th.start()
-        for th in ths:
-            th.join()
+                done.put(None)
+            except Exception as e:  # surfaced by run()
+                done.put(e)
+
+    ths = [threading.Thread(target=worker, args=(i,) + sl, daemon=True) for i, sl in enumerate(slices)]
+    for th in ths:
+        th.start()
+
+    def run(nsteps):
+        for q_ in cmds:
+            q_.put(nsteps)
+        errs = [done.get() for _ in cmds]
+        errs = [e for e in errs if e is not None]
         if errs:
             raise errs[0]
 
@@ -804,6 +820,10 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
         run(args.steps)
         reps.append(max_over_ranks(time.perf_counter() - t0, world))
     el = sorted(reps)[len(reps) // 2]
+    for q_ in cmds:
+        q_.put(None)
+    for th in ths:
+        th.join()
     tb = B * H * N * D * es
     h2d = layers * (3 * tb + B * N) + layers * tb  # fwd: Q, K, V, mask; bwd: dO
     d2h = layers * tb + layers * 3 * tb            # fwd: O; bwd: dQ, dK, dV
