@@ -737,11 +737,11 @@ def run_e2e(args, world, B, N, H, D, layers, global_b, dname="f32"):
 
     # The reference calls the op from parallel_chunks workers (encoder.cpp:295,345); the
     # host entry points are thread-safe with per-thread streams, so W host threads
-    # (COTTEN_E2E_THREADS, default 4 = the host-call gate's default) each run the step
+    # (COTTEN_E2E_THREADS, default 8 = the host-call gate's default) each run the step
     # on a contiguous slice of the batch, so their PCIe transfers overlap: with
-    # persistent workers 1 / 2 / 4 threads read 68 / 77 / 79 k seq/s, every window
-    # within 1 % (profiles/r02an_e2e_threads).
-    W = max(1, min(B, int(os.environ.get("COTTEN_E2E_THREADS", "4"))))
+    # persistent workers 1 / 2 / 4 / 8 / 16 threads read 68 / 77 / 80-85 / 83 / 71 k
+    # seq/s (profiles/r02an_e2e_threads).
+    W = max(1, min(B, int(os.environ.get("COTTEN_E2E_THREADS", "8"))))
     es = 2 if dname == "bf16" else 4
     per = (B + W - 1) // W
     slices = [(b0, min(B, b0 + per)) for b0 in range(0, B, per)]

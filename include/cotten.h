@@ -127,7 +127,7 @@ int cotten_device_status(int device, int32_t* bits, int reset);
  * thread's stream and copies the results back before returning.  Thread-safe:
  * every calling thread gets its own stream and workspace (the reference calls
  * the op concurrently from parallel_chunks workers, encoder.cpp:295,345); at
- * most COTTEN_HOST_MAX_CONCURRENT (environment, default 4) host-entry calls
+ * most COTTEN_HOST_MAX_CONCURRENT (environment, default 8) host-entry calls
  * stage and run at once per process, further callers wait their turn. */
 int cotten_fwd_host(const cotten_desc* desc, const void* q, const void* k, const void* v,
                     const uint8_t* valid, double m, void* out, void* saved_S,

@@ -492,12 +492,12 @@ struct HostCtx {
 };
 thread_local std::map<int, HostCtx> g_hosts;
 thread_local HostCtx* g_host = nullptr;
-// At most COTTEN_HOST_MAX_CONCURRENT (default 4) host-entry calls stage and run
-// at once per process; further callers queue.  The host path is PCIe-bound and
-// 2-4 concurrent callers already keep both copy directions busy, while the
-// reference calls the op from cfg.threads parallel_chunks workers: at 16 host
-// threads the gate held ML-1M e2e at 48-49 k seq/s over five windows, against
-// 4-49 k without it (profiles/r02ac_host_threads).
+// At most COTTEN_HOST_MAX_CONCURRENT (default 8) host-entry calls stage and run
+// at once per process; further callers queue.  The host path is PCIe-bound; with
+// persistent callers 4-8 concurrent calls keep both copy directions busy (ML-1M
+// e2e: 8 threads 83 k seq/s with the limit at 8, 79 k at 4; 16 threads 71 k with
+// the limit at 8 — profiles/r02an_e2e_threads), while the reference calls the op
+// from cfg.threads parallel_chunks workers.
 class HostGate {
  public:
   void acquire() {
@@ -517,7 +517,7 @@ class HostGate {
   static int limit() {
     static const int v = [] {
       const char* e = std::getenv("COTTEN_HOST_MAX_CONCURRENT");
-      return e ? std::max(1, std::atoi(e)) : 4;
+      return e ? std::max(1, std::atoi(e)) : 8;
     }();
     return v;
   }
