@@ -199,7 +199,7 @@ def test_cached_backward_on_another_thread_and_pool_reuse():
 
 
 def test_many_host_threads_through_the_gate():
-    """12 threads (more than the default 4 concurrent host calls the gate
+    """12 threads (more than the default 8 concurrent host calls the gate
     admits) each run cached fwd + bwd on their own batch slice, 3 times; every
     slice equals the same call made alone, and nothing deadlocks."""
     import threading
