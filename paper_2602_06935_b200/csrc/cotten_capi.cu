@@ -490,7 +490,28 @@ struct HostCtx {
     return bufs[slot];
   }
 };
-thread_local std::map<int, HostCtx> g_hosts;
+// Staging contexts outlive the threads that used them: a thread's contexts go back
+// to a process-wide pool when it exits and the next new thread takes one from
+// there.  The reference calls the op from short-lived parallel_chunks workers
+// (encoder.cpp:295,345); with a context per thread every such call paid 4 x
+// cudaStreamCreate, the staging cudaMallocs and, at thread exit, a device-
+// synchronising cudaFree (measured from the bench's e2e with threads created per
+// window: single windows fell from 70 k to 6-20 k seq/s, profiles/r02an_e2e_threads).
+// The pool is never destroyed (process teardown may already have torn the CUDA
+// context down).
+struct HostPool {
+  std::mutex mu;
+  std::map<int, std::vector<HostCtx*>> free;
+};
+HostPool* g_hpool = new HostPool;
+struct ThreadHosts {
+  std::map<int, HostCtx*> ctx;
+  ~ThreadHosts() {
+    std::lock_guard<std::mutex> lk(g_hpool->mu);
+    for (auto& kv : ctx) g_hpool->free[kv.first].push_back(kv.second);
+  }
+};
+thread_local ThreadHosts g_hosts;
 thread_local HostCtx* g_host = nullptr;
 // At most COTTEN_HOST_MAX_CONCURRENT (default 8) host-entry calls stage and run
 // at once per process; further callers queue.  The host path is PCIe-bound; with
@@ -536,7 +557,19 @@ struct HostSlot {
 void host_begin() {
   int cur = 0;
   COTTEN_CUDA(cudaGetDevice(&cur));
-  g_host = &g_hosts[cur];
+  HostCtx*& h = g_hosts.ctx[cur];
+  if (h == nullptr) {
+    {
+      std::lock_guard<std::mutex> lk(g_hpool->mu);
+      std::vector<HostCtx*>& f = g_hpool->free[cur];
+      if (!f.empty()) {
+        h = f.back();
+        f.pop_back();
+      }
+    }
+    if (h == nullptr) h = new HostCtx;
+  }
+  g_host = h;
   g_host->ensure(cur);
 }
 
