@@ -96,6 +96,25 @@ using tch::kRun;
 using tch::kTmemCols;
 using tch::out_col;
 
+// Optional per-item trace of the backward (-DCOTTEN_TCG_TRACE=1, variant builds
+// only): clock64 stamps of the first tcb::kTraceItems items of every CTA into
+// p.workspace [cta][item][8], the stamp meanings of kernels_tcb.cuh
+// (scripts/dev/tcb_trace_report.py reads tcg_bwd.bin).
+#ifndef COTTEN_TCG_TRACE
+#define COTTEN_TCG_TRACE 0
+#endif
+#if COTTEN_TCG_TRACE
+#define TCG_TRACE(k, cond)                                                                   \
+  do {                                                                                       \
+    if ((cond) && p.workspace && it < tcb::kTraceItems)                                      \
+      static_cast<long long*>(p.workspace)[(blockIdx.x * tcb::kTraceItems + it) * 8 + (k)] = clock64(); \
+  } while (0)
+#else
+#define TCG_TRACE(k, cond) \
+  do {                     \
+  } while (0)
+#endif
+
 __device__ __forceinline__ int slot2(int it) { return it & 1; }
 __device__ __forceinline__ uint32_t par2(int it) { return (uint32_t)(it >> 1) & 1u; }
 
@@ -561,6 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcg_kernel(
         for (int c = 0; c < C; ++c, ++it) {
           const int st = slot2(it);
           mbar_wait(&br->split_full[st], par2(it));
+          TCG_TRACE(3, lane == 0);
           if (ps == 1 && c == 0) mbar_wait(&br->op_ready, j & 1);
           if (ps == 0 && c > 0 && c % kFlush == 0) mbar_wait(&br->acc_free, (nflush++) & 1);
           if (ps == 0 && c == 0) mbar_wait(&br->out_free[2], ((par >> 2) & 1u) ^ 1u);
@@ -598,6 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcg_kernel(
             }
             __syncwarp();
           }
+          TCG_TRACE(4, lane == 0);
         }
     }
   } else if (warp == kWarpMask) {
@@ -622,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcg_kernel(
             }
             bulk_wait_read0();
             mbar_arrive(&br->slot_free[st]);
+            TCG_TRACE(7, true);
           }
       }
       tc::store_tail();
@@ -668,7 +690,9 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcg_kernel(
               store_state_block(ops, a, 2 * hh + r, v);
             }
           }
+          TCG_TRACE(0, threadIdx.x == 0);
           mbar_wait(&br->raw_full[st], par2(it));
+          TCG_TRACE(1, threadIdx.x == 0);
           SplitRow s, y;
           split_load(X, t, s);
           split_load(Y, t, y);
@@ -690,6 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcg_kernel(
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&br->split_full[st]);
+          TCG_TRACE(2, threadIdx.x == 0);
         } else {  // ---------------- epiloguer ----------------
           if (ps == 0 && c == C - 1) {
             // G complete: dm = -ln(n) s <G, S> (:408); dA = s G (:412-413) over S in place
@@ -720,6 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcg_kernel(
             }
           }
           mbar_wait(&br->mma_done[st], par2(it));
+          TCG_TRACE(5, t == 0);
           tc_fence_after();
           if (ps == 0 && c != C - 1 && c % kFlush == kFlush - 1) {  // long N: flush G
             flush_acc(tmem, lane_base, c == kFlush - 1);
@@ -801,6 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1) cos_bwd_tcg_kernel(
             ++n2;
           }
           arrive_staged(br, st, lane);
+          TCG_TRACE(6, t == 0);
         }
       }
       __syncwarp();
@@ -893,8 +920,25 @@ inline int launch_tcg_bwd(const OpParams& p, cudaStream_t st) {
   const int grid = std::min((int)(p.B * p.H), sm_count());
   OpParams q = p;
   q.l2_ahead = l2_ahead_items();
+#if COTTEN_TCG_TRACE
+  static void* tbuf = nullptr;
+  if (!tbuf) cudaMalloc(&tbuf, (size_t)1024 * tcb::kTraceItems * 8 * sizeof(long long));
+  cudaMemsetAsync(tbuf, 0, (size_t)grid * tcb::kTraceItems * 8 * sizeof(long long), st);
+  q.workspace = tbuf;
+#endif
   if (launch_tcg_pdl(tcg::cos_bwd_tcg_kernel, grid, st, mq, mk, mv, mg, mdq, mdk, mdv, q) != cudaSuccess)
     return -1;
+#if COTTEN_TCG_TRACE
+  if (const char* dir = getenv("COTTEN_TRACE_DIR")) {
+    std::vector<long long> h((size_t)grid * tcb::kTraceItems * 8);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), tbuf, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen((std::string(dir) + "/tcg_bwd.bin").c_str(), "wb")) {
+      fwrite(h.data(), sizeof(long long), h.size(), f);
+      fclose(f);
+    }
+  }
+#endif
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -6,7 +6,7 @@ import numpy as np
 K = 64
 names = ["split wait raw", "raw landed", "split published", "mma sees split", "mma issued",
          "epi sees done", "epi staged", "slot freed"]
-for tag in ("tcb_fwd", "tcb_bwd"):
+for tag in ("tcb_fwd", "tcb_bwd", "tcg_bwd"):
     try:
         a = np.fromfile(f"{sys.argv[1]}/{tag}.bin", dtype=np.int64).reshape(-1, K, 8).astype(np.float64)
     except FileNotFoundError:
